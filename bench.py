@@ -1,0 +1,369 @@
+#!/usr/bin/env python
+"""Benchmark of the gate-application hot path (BASELINE.json metric).
+
+Default workload (N=1: BASELINE config 2): n = 30 + log2(N) qubits, 2^30
+complex128 amplitudes (16 GiB) per GPU, seeded random normalised state; one
+step = one per-target sweep, a fresh Haar-random 2x2 unitary on every qubit
+k = 0..n-1 in order (at N > 1 the top log2(N) targets are global qubits and
+run the fused NVLink exchange).  Weak scaling: per-GPU work is fixed.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload sweep|controlled|random|qft] [--n N]
+
+Prints ONE JSON line on rank 0.  `value` is the effective HBM bandwidth per
+gate of the whole job, (gates x 32 x 2^n bytes) / time, the paper's
+"effective GB/s per gate"; `gates_per_s` rides along.
+Timing: W untimed steps, then K steps between barrier+synchronize, CUDA
+events on the launching stream, max over ranks.  The 16 GiB slice is ~130x
+the 126 MB L2, so no flush is needed between steps.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "gates/sec & effective HBM GB/s per gate vs 8 TB/s at n qubits; 1/2/4/8 GPU"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=["sweep", "controlled", "random", "qft"], default="sweep")
+    ap.add_argument("--n", type=int, default=None, help="total qubits (default 30 + log2(N))")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--out", default=None, help="also write the JSON line here")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def step_circuits(sv, workload, n, count, seed=1):
+    """One circuit per step (fresh Haar gates each step, same placement)."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(count):
+        if workload == "sweep":
+            out.append(sv.per_target_sweep(n, 1, rng))
+        elif workload == "controlled":  # BASELINE config 3 shape, 30 gates per step
+            out.append(sv.random_circuit(n, 30, rng, controlled_fraction=1.0))
+        elif workload == "random":  # BASELINE config 4 shape, 25 gates per step
+            out.append(sv.random_circuit(n, 25, rng, controlled_fraction=0.0))
+        else:
+            out.append(sv.build_qft(n))
+    return out
+
+
+def effective_bytes(circ, n):
+    """Paper's effective bytes per gate: 32 x 2^n (16 x 2^n for controlled)."""
+    return sum((32 if op.control is None else 16) << n for op in circ)
+
+
+class ClockSampler:
+    """nvidia-smi-equivalent sampling (NVML) of SM clocks / throttle reasons during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.ok = [], 0, False
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(0.05)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max, "reasons": ["unavailable"]}
+        names = [v for k, v in self.REASONS.items() if self.reasons & k and v != "gpu_idle"]
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max, "reasons": names,
+                "samples": len(self.samples)}
+
+
+def load_peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text()), "measured"
+    except (OSError, ValueError):
+        return {"hbm_gbs": 6650.0}, "fallback"
+
+
+def ncu_traffic(kernel_key):
+    """dram bytes per launch of the dominant kernel from the committed ncu --set full summary."""
+    try:
+        d = json.loads((ROOT / "profiles" / "ncu_summary.json").read_text())
+        return d["kernels"][kernel_key]["dram_bytes_per_launch"]
+    except (OSError, KeyError, ValueError, TypeError):
+        return None
+
+
+def cpu_baseline(sv, host_state, n, circ, seconds):
+    """The oracle (C restatement of the reference's kernels, OpenMP) on the host copy of the state."""
+    from oracle import oracle
+
+    threads = os.cpu_count() or 1
+    amps = host_state.numpy() if hasattr(host_state, "numpy") else host_state
+    gates = 0
+    nbytes = 0
+    t0 = time.perf_counter()
+    for op in circ:
+        oracle.apply_gate(amps, op, threads=threads)
+        gates += 1
+        nbytes += (32 if op.control is None else 16) << n
+        if time.perf_counter() - t0 > seconds:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": round(nbytes / dt / 1e9, 3), "unit": "GB/s", "cores": threads, "kind": "port",
+            "gates_per_s": round(gates / dt, 4),
+            "sample": f"first {gates} gates (targets {circ.gates[0].target}..{circ.gates[gates - 1].target}) "
+                      f"of one n={n} step on the host copy of the state, oracle/sv_oracle.c with {threads} "
+                      f"OpenMP threads, {dt:.2f} s"}
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU algorithm (oracle port, all host threads) on our config."""
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import paper_1601_07195_b200 as sv
+    from oracle import oracle
+
+    g = world.bit_length() - 1
+    n = args.n or (30 + g)
+    threads = os.cpu_count() or 1
+    amps = np.empty(1 << n, dtype=np.complex128)
+    oracle.fill_phase(amps, threads)
+    circs = step_circuits(sv, args.workload, n, 1)
+    pool = circs[0].gates
+    times, eff = [], 0
+    for s in range(args.warmup + args.steps):
+        op = pool[(s * 7) % len(pool)]
+        t0 = time.perf_counter()
+        oracle.apply_gate(amps, op, threads=threads)
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            times.append(dt)
+            eff += (32 if op.control is None else 16) << n
+    tot = sum(times)
+    value = eff / tot / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(tot / args.steps * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "gates_per_s": round(args.steps / tot, 4),
+        "config": {"workload": f"{args.workload} n={n} (BASELINE config 2 at N=1)", "n_qubits": n,
+                   "sample": "one gate of the step per timed step, target k = 7*s mod n"},
+        "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": threads, "kind": "port",
+                         "sample": f"{args.steps} single gates of the n={n} sweep on a host state, "
+                                   f"oracle/sv_oracle.c (C restatement of kernels.py:120-196), {threads} threads"},
+        "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    import paper_1601_07195_b200 as sv
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    fabric = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        fabric = sv.NvlinkFabric()
+    if world & (world - 1):
+        raise SystemExit("--gpus must be a power of two")
+    g = world.bit_length() - 1
+    n = args.n or (30 + g)
+    lay = sv.Layout(n, g, rank)
+    m = lay.m
+    circs = step_circuits(sv, args.workload, n, args.warmup + args.steps)
+    state = sv.init_random_state(lay, seed=0, transport=fabric, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    # ---------------------------------------------------------- warm-up
+    for c in circs[: args.warmup]:
+        sv.run_circuit(state, c, fabric)
+    barrier()
+
+    # ------------------------------------------------ timed (device-resident)
+    timed = circs[args.warmup:]
+    ev = []
+    launches0 = sv.launch_count()
+    with ClockSampler(local) as clocks:
+        barrier()
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        for c in timed:
+            row = [torch.cuda.Event(enable_timing=True)]
+            row[0].record(stream)
+            for op in c:
+                sv.apply_op(state, op, fabric)
+                e = torch.cuda.Event(enable_timing=True)
+                e.record(stream)
+                row.append(e)
+            ev.append(row)
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    launches = sv.launch_count() - launches0
+    elapsed_ms = t_start.elapsed_time(t_end)
+    if world > 1:
+        t = torch.tensor([elapsed_ms, float(launches)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t[:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(t[1:], op=dist.ReduceOp.SUM)
+        elapsed_ms, launches = float(t[0]), int(t[1])
+    gate_ms = np.array([[row[i].elapsed_time(row[i + 1]) for i in range(len(row) - 1)] for row in ev])
+    ngates = sum(len(c) for c in timed)
+    eff = sum(effective_bytes(c, n) for c in timed)
+    value = eff / (elapsed_ms * 1e-3) / 1e9
+
+    # roofline of the dominant kernel: local single-qubit update (sv_apply_single)
+    peaks, peak_kind = load_peaks()
+    local_single = [(j, i) for j, c in enumerate(timed) for i, op in enumerate(c)
+                    if op.control is None and op.target < m]
+    per_target = {}
+    roof = None
+    if local_single:
+        d = np.array([gate_ms[j][i] for j, i in local_single])
+        avg_ms = float(d.mean())
+        achieved = (32 << m) / (avg_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": ncu_traffic("sv_apply_single"),
+                "kernel": "k_pairs/k_shfl<MODE_SINGLE> (sv_apply_single)", "peak_kind": peak_kind,
+                "algorithmic_bytes_per_launch": 32 << m, "avg_launch_ms": round(avg_ms, 4),
+                "frac_of_8TBs": round(achieved / 8000.0, 4)}
+        if args.workload == "sweep":
+            for k in range(m):
+                ks = [gate_ms[j][k] for j in range(len(timed))]
+                per_target[k] = round((32 << m) / (float(np.median(ks)) * 1e-3) / 1e9, 1)
+    nvlink = None
+    if world > 1:
+        glob = [(j, i) for j, c in enumerate(timed) for i, op in enumerate(c) if op.max_qubit() >= m]
+        if glob:
+            d = np.array([gate_ms[j][i] for j, i in glob])
+            per_dir = 1 << (m + 4)
+            nvlink = {"achieved_gbs_per_direction": round(per_dir / (float(d.mean()) * 1e-3) / 1e9, 1),
+                      "peak_nominal": 900.0, "peak_measured_ref": 770.0,
+                      "frac_nominal": round(per_dir / (float(d.mean()) * 1e-3) / 1e9 / 900.0, 4),
+                      "global_gates_per_step": len(glob) // len(timed), "avg_gate_ms": round(float(d.mean()), 3)}
+
+    # ---------------------------------------------- end to end (host buffers)
+    e2e = None
+    cpu = None
+    if not args.no_e2e:
+        host = torch.empty(lay.local_len, dtype=torch.complex128, pin_memory=True)
+        state.store_host(host)
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for c in timed:
+            state.load_host(host)                 # H2D of the step's input state
+            sv.run_circuit(state, c, fabric)
+            state.store_host(host)                # D2H of the step's result
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t[0])
+        e2e = {"value": round(eff / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
+               "h2d_bytes_per_step": (16 << m) * world, "d2h_bytes_per_step": (16 << m) * world,
+               "ms_per_step": round(e2e_ms / len(timed), 3),
+               "path": "LocalState.load_host -> run_circuit -> LocalState.store_host (sv_copy + kernels)"}
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            cpu = cpu_baseline(sv, host, n, timed[0], args.cpu_seconds)
+        del host
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(elapsed_ms / args.steps, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+            "gates_per_s": round(ngates / (elapsed_ms * 1e-3), 3),
+            "config": {"workload": f"{args.workload}: n={n}, one fresh Haar gate per target k=0..{n - 1} per step"
+                       if args.workload == "sweep" else f"{args.workload}: n={n}",
+                       "n_qubits": n, "local_qubits": m, "global_qubits": g, "gates_per_step": len(timed[0]),
+                       "state_gib_per_gpu": (16 << m) / 2**30, "parallelism": f"state sharded over {world} GPU(s)",
+                       "l2": "no flush: 16 GiB slice >> 126 MB L2", "seed": {"state": 0, "circuit": 1}},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clocks.summary(),
+        }
+        if per_target:
+            line["per_target_gbps"] = per_target
+        if nvlink:
+            line["nvlink"] = nvlink
+        s = json.dumps(line)
+        print(s, flush=True)
+        if args.out:
+            Path(args.out).write_text(s + "\n")
+    if fabric is not None:
+        fabric.close()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,122 @@
+/*
+ * svb200.h -- C ABI of the B200-native gate-application hot path.
+ *
+ * The reference (qHiPSTER restated as the Python package `svsim`) has no FFI:
+ * its hot path sits behind Python functions.  Each entry point below is the
+ * drop-in for one of those functions; the host mirror in
+ * paper_1601_07195_b200/ binds them with ctypes, validates arguments first
+ * (raising the reference's exception types) and passes plain device pointers,
+ * sizes and a cudaStream_t.  No torch types cross this boundary.
+ *
+ * Conventions (all entry points):
+ *   - amplitudes are complex128 = interleaved (re, im) float64 = CUDA double2,
+ *     16-byte aligned, 2^m contiguous elements (pkg/src/svsim/core.py:67-75);
+ *   - updates are in place, stream-ordered and asynchronous; the caller owns
+ *     every buffer (core.py LocalState; SURVEY.md 8b "conventions to keep");
+ *   - a gate matrix is 8 doubles q11re q11im q12re q12im q21re q21im q22re q22im
+ *     (row-major 2x2, pkg/src/svsim/kernels.py:36-68);
+ *   - return 0 on success, SV_EINVAL for a rejected argument, SV_ECUDA for a
+ *     CUDA launch/runtime error; sv_last_error() holds the message (per thread).
+ *   - arithmetic reproduces the reference's rounding sequence exactly
+ *     (kernels.py:120-131 mix()).
+ */
+#ifndef SVB200_H
+#define SVB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SV_OK 0
+#define SV_EINVAL (-1)
+#define SV_ECUDA (-2)
+
+/* Largest fused tile exponent: one CTA keeps 2^SV_FUSED_MAX_TILE amplitudes
+ * (128 KiB) resident in shared memory. */
+#define SV_FUSED_MAX_TILE 13
+/* Gates carried by one fused launch (kernel parameter space). */
+#define SV_FUSED_MAX_GATES 256
+/* Scratch doubles sv_norm_sq needs (per-block partials + result). */
+#define SV_NORM_SCRATCH 1025
+
+/* One gate of a fused run: `control` = -1 for an uncontrolled gate.
+ * Mirrors svsim GateOp (pkg/src/svsim/circuits.py:71-99). */
+typedef struct {
+  int32_t target;
+  int32_t control;
+  double q[8];
+} sv_gate;
+
+int sv_version(void);
+const char *sv_last_error(void);
+/* Number of CUDA kernels this library has launched (process lifetime). */
+uint64_t sv_launch_count(void);
+
+/* Replaces svsim.kernels.apply_single_raw (pkg/src/svsim/kernels.py:187-189):
+ * pairs (i, i + 2^k) with bit k of i clear, 0 <= k < m. */
+int sv_apply_single(void *amps, int m, int k, const double *q, void *stream);
+
+/* Replaces svsim.kernels.apply_controlled_raw (kernels.py:192-196): pairs with
+ * bit c set and bit t in {0,1}; c != t, both < m.  Touches only the bit-c = 1
+ * half of the slice. */
+int sv_apply_controlled(void *amps, int m, int c, int t, const double *q, void *stream);
+
+/* Replaces the FusedBlockRun branch of svsim.fusion.execute_plan
+ * (pkg/src/svsim/fusion.py:124-135), i.e. apply_block (kernels.py:225-240) on
+ * every contiguous 2^l block: the gates are applied in order to each block
+ * while it stays resident in shared memory, one HBM pass per launch.
+ * Requires 1 <= l <= min(m, SV_FUSED_MAX_TILE), every gate qubit < l,
+ * 1 <= ngates <= SV_FUSED_MAX_GATES. */
+int sv_apply_fused(void *amps, int m, int l, const sv_gate *gates, int ngates, void *stream);
+
+/* Replaces one rank's side of the half exchange:
+ * svsim.distributed._run_exchange + chunked_exchange_pipeline + _pair_kernel
+ * (pkg/src/svsim/distributed.py:187-311) and the packed remote-target case
+ * (:404-422).  `theirs` is the partner's slice mapped into this process
+ * (sv_ipc_open), so transfer and update are one kernel: each element of the
+ * computed half is read from both slices, the kept value is stored locally and
+ * the returned value is stored straight into the partner's slice over NVLink.
+ * own_is_zero selects the computed half (first half on the zero side);
+ * c_local = -1 exchanges every element, c_local in [0, m) only those with
+ * local bit c_local set (case 5 of perfmodel.py:30-38; c_local = m-1 leaves the
+ * zero side idle, as distributed.py:348-349).  The caller orders the launch
+ * between two partner barriers. */
+int sv_exchange(void *mine, void *theirs, int m, int own_is_zero, int c_local, const double *q,
+                void *stream);
+
+/* Sum of |a|^2 over the slice (qubit = -1) or over local bit `qubit` = 1
+ * (core.py:147-167 partials).  Deterministic: fixed grid, fixed reduction
+ * order.  `scratch` is a device buffer of SV_NORM_SCRATCH doubles; the result
+ * lands in scratch[SV_NORM_SCRATCH - 1]. */
+int sv_norm_sq(const void *amps, int m, int qubit, double *scratch, void *stream);
+
+/* Seeded i.i.d. complex Gaussian amplitudes (Philox4x32-10 + Box-Muller),
+ * element j of rank r drawn from counter (r << m) + j, so a sharded state
+ * equals the unsharded one.  Not normalised: follow with sv_norm_sq/sv_scale. */
+int sv_init_random(void *amps, int m, uint64_t seed, uint64_t rank, void *stream);
+
+/* amps *= s (real scale). */
+int sv_scale(void *amps, int m, double s, void *stream);
+
+/* |basis> on this slice: zero everything, amps[local] = 1 if local >= 0. */
+int sv_init_basis(void *amps, int m, int64_t local, void *stream);
+
+/* Stream-ordered byte copy between any two UVA addresses (device, mapped
+ * peer, pinned host): gather_full_state's NVLink read (distributed.py:462-482). */
+int sv_copy(void *dst, const void *src, uint64_t nbytes, void *stream);
+
+/* CUDA IPC for the exchange data plane (replaces the Transport ABC's byte
+ * channel, distributed.py:60-92).  handle_out receives 64 bytes; offset_out the
+ * byte offset of ptr inside its allocation. */
+int sv_ipc_handle(const void *ptr, void *handle_out, uint64_t *offset_out);
+int sv_ipc_open(const void *handle, uint64_t offset, void **ptr_out);
+int sv_ipc_close(void *ptr, uint64_t offset);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SVB200_H */

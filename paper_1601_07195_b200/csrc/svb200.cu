@@ -1,0 +1,581 @@
+// svb200.cu -- hand-written sm_100a kernels + C ABI for the gate-application hot path.
+//
+// See include/svb200.h for the ABI contract and DESIGN.md for the data layout,
+// the roofline each kernel is held to and the parity argument.  Every kernel
+// that touches amplitudes evaluates the reference's pair update
+// (pkg/src/svsim/kernels.py:120-131) with the rounding sequence numpy uses:
+//
+//   cmul(r, a)  = ( fma(r.re, a.re, -(a.im*r.im)),  fma(r.re, a.im, a.re*r.im) )
+//   mix(a0,a1,r0,r1) = cmul(r0,a0) + cmul(r1,a1)      (componentwise add)
+//
+// written with __fma_rn/__dmul_rn/__dadd_rn so nvcc cannot re-associate or
+// contract differently; results are bit-identical to the reference and to
+// oracle/sv_oracle.c, and independent of launch geometry, fusion and sharding.
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+
+#include "svb200.h"
+
+#define SV_ABI_VERSION 1
+
+namespace {
+
+thread_local char g_err[512] = "";
+std::atomic<uint64_t> g_launches{0};
+
+int fail(int code, const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int after_launch(const char *what, int nlaunch = 1) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(SV_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+  g_launches.fetch_add((uint64_t)nlaunch, std::memory_order_relaxed);
+  return SV_OK;
+}
+
+struct GateQ {
+  double v[8];  // q11re q11im q12re q12im q21re q21im q22re q22im
+};
+
+GateQ load_q(const double *q) {
+  GateQ g;
+  memcpy(g.v, q, sizeof(g.v));
+  return g;
+}
+
+// ------------------------------------------------------------------ arithmetic
+
+__device__ __forceinline__ double2 cmul(double rr, double ri, double2 a) {
+  return make_double2(__fma_rn(rr, a.x, -__dmul_rn(a.y, ri)), __fma_rn(rr, a.y, __dmul_rn(a.x, ri)));
+}
+
+__device__ __forceinline__ double2 mix(double2 a0, double2 a1, double r0r, double r0i, double r1r,
+                                       double r1i) {
+  const double2 x = cmul(r0r, r0i, a0);
+  const double2 y = cmul(r1r, r1i, a1);
+  return make_double2(__dadd_rn(x.x, y.x), __dadd_rn(x.y, y.y));
+}
+
+__device__ __forceinline__ uint64_t insert_zero(uint64_t x, int b) {
+  const uint64_t lo = x & ((1ull << b) - 1ull);
+  return ((x >> b) << (b + 1)) | lo;
+}
+
+__device__ __forceinline__ uint64_t insert_one(uint64_t x, int b) { return insert_zero(x, b) | (1ull << b); }
+
+__device__ __forceinline__ double2 shfl_xor2(double2 v, int mask) {
+  return make_double2(__shfl_xor_sync(0xffffffffu, v.x, mask), __shfl_xor_sync(0xffffffffu, v.y, mask));
+}
+
+// ---------------------------------------------------------------- local kernels
+//
+// Index spaces.  MODE_SINGLE: the slice itself, pairs on bit tv.
+// MODE_CTL: the 2^(m-1) "virtual" elements with bit c set (virtual index v maps
+// to insert_one(v, c)); the gate is a single-qubit gate on virtual bit tv
+// (tv = t if t < c else t-1), so the kernel reads and writes only the
+// control-set half.  MODE_PRED (c = 0, where control-set elements interleave
+// at 16 B inside every 32-B sector): the full slice is streamed, pairs whose
+// bit c is clear are written back unchanged, so every sector is read and
+// written whole instead of half-used.
+
+constexpr int BLK = 256;
+constexpr int UNROLL = 4;
+enum { MODE_SINGLE = 0, MODE_CTL = 1, MODE_PRED = 2 };
+
+template <int MODE>
+__device__ __forceinline__ uint64_t vmap(uint64_t v, int c) {
+  return MODE == MODE_CTL ? insert_one(v, c) : v;
+}
+
+// Pair mode (tv >= 5): each thread owns UNROLL pairs; a warp's 32 consecutive
+// pairs give two fully coalesced 512-B streams (a[i0], a[i0 + 2^tv]).
+template <int MODE>
+__global__ void __launch_bounds__(BLK) k_pairs(double2 *__restrict__ a, uint64_t npairs, int tv, int c,
+                                               GateQ q) {
+  const uint64_t tb = 1ull << tv;
+  const uint64_t p0 = (uint64_t)blockIdx.x * (BLK * UNROLL) + threadIdx.x;
+  double2 x0[UNROLL], x1[UNROLL];
+  uint64_t i0[UNROLL], i1[UNROLL];
+#pragma unroll
+  for (int u = 0; u < UNROLL; ++u) {
+    const uint64_t p = p0 + (uint64_t)u * BLK;
+    const uint64_t v0 = insert_zero(p, tv);
+    i0[u] = vmap<MODE>(v0, c);
+    i1[u] = vmap<MODE>(v0 | tb, c);
+    if (p < npairs) {
+      x0[u] = a[i0[u]];
+      x1[u] = a[i1[u]];
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < UNROLL; ++u) {
+    const uint64_t p = p0 + (uint64_t)u * BLK;
+    if (p >= npairs) continue;
+    double2 n0 = mix(x0[u], x1[u], q.v[0], q.v[1], q.v[2], q.v[3]);
+    double2 n1 = mix(x0[u], x1[u], q.v[4], q.v[5], q.v[6], q.v[7]);
+    if (MODE == MODE_PRED && !((i0[u] >> c) & 1ull)) {
+      n0 = x0[u];
+      n1 = x1[u];
+    }
+    a[i0[u]] = n0;
+    a[i1[u]] = n1;
+  }
+}
+
+// Shuffle mode (tv < 5): a warp streams 32 consecutive (virtual) elements per
+// unroll step; the pair partner sits in lane ^ 2^tv.  Each lane produces one
+// output with the operand order of the reference (a0 = bit-clear element).
+template <int MODE>
+__global__ void __launch_bounds__(BLK) k_shfl(double2 *__restrict__ a, uint64_t nvirt, int tv, int c,
+                                              GateQ q) {
+  const int lane = threadIdx.x & 31;
+  const bool hi = (lane >> tv) & 1;
+  const double r0r = hi ? q.v[4] : q.v[0], r0i = hi ? q.v[5] : q.v[1];
+  const double r1r = hi ? q.v[6] : q.v[2], r1i = hi ? q.v[7] : q.v[3];
+  const int mask = 1 << tv;
+  const uint64_t v0 = (uint64_t)blockIdx.x * (BLK * UNROLL) + threadIdx.x;
+  double2 x[UNROLL];
+  uint64_t idx[UNROLL];
+#pragma unroll
+  for (int u = 0; u < UNROLL; ++u) {
+    const uint64_t v = v0 + (uint64_t)u * BLK;
+    idx[u] = vmap<MODE>(v, c);
+    if (v < nvirt) x[u] = a[idx[u]];  // warp-uniform: nvirt is a multiple of 32
+  }
+#pragma unroll
+  for (int u = 0; u < UNROLL; ++u) {
+    const uint64_t v = v0 + (uint64_t)u * BLK;
+    if (v >= nvirt) continue;
+    const double2 o = shfl_xor2(x[u], mask);
+    const double2 a0 = hi ? o : x[u];
+    const double2 a1 = hi ? x[u] : o;
+    double2 r = mix(a0, a1, r0r, r0i, r1r, r1i);
+    if (MODE == MODE_PRED && !((idx[u] >> c) & 1ull)) r = x[u];
+    a[idx[u]] = r;
+  }
+}
+
+// ------------------------------------------------------------------ fused runs
+//
+// One CTA per 2^T tile: coalesced 16-B loads into shared memory, the run's
+// gates applied in order on the resident tile (one __syncthreads per gate),
+// one coalesced store.  One HBM read + write of the slice per launch no matter
+// how many gates the run holds.
+
+struct FusedParams {
+  int ngates;
+  int pad;
+  sv_gate g[SV_FUSED_MAX_GATES];
+};
+
+template <int T>
+struct FusedShape {
+  static constexpr int NT = (T >= 10) ? 512 : ((1 << (T - 1)) < 32 ? 32 : (1 << (T - 1)));
+  static constexpr int N = 1 << T;
+};
+
+template <int T>
+__global__ void __launch_bounds__(FusedShape<T>::NT) k_fused(double2 *__restrict__ a, const FusedParams P) {
+  constexpr int NT = FusedShape<T>::NT;
+  constexpr int N = FusedShape<T>::N;
+  extern __shared__ double2 s[];
+  double2 *__restrict__ g = a + ((uint64_t)blockIdx.x << T);
+  const int tid = threadIdx.x;
+#pragma unroll
+  for (int i = tid; i < N; i += NT) s[i] = g[i];
+  __syncthreads();
+  for (int gi = 0; gi < P.ngates; ++gi) {
+    const int t = P.g[gi].target, c = P.g[gi].control;
+    const double q0 = P.g[gi].q[0], q1 = P.g[gi].q[1], q2 = P.g[gi].q[2], q3 = P.g[gi].q[3];
+    const double q4 = P.g[gi].q[4], q5 = P.g[gi].q[5], q6 = P.g[gi].q[6], q7 = P.g[gi].q[7];
+    const int tb = 1 << t;
+    if (c < 0) {
+      for (int p = tid; p < (N >> 1); p += NT) {
+        const int i0 = (int)insert_zero((uint64_t)p, t);
+        const double2 x0 = s[i0], x1 = s[i0 | tb];
+        s[i0] = mix(x0, x1, q0, q1, q2, q3);
+        s[i0 | tb] = mix(x0, x1, q4, q5, q6, q7);
+      }
+    } else {
+      const int lo = c < t ? c : t, hi = c < t ? t : c;
+      for (int p = tid; p < (N >> 2); p += NT) {
+        const int i0 = (int)insert_zero(insert_zero((uint64_t)p, lo), hi) | (1 << c);
+        const double2 x0 = s[i0], x1 = s[i0 | tb];
+        s[i0] = mix(x0, x1, q0, q1, q2, q3);
+        s[i0 | tb] = mix(x0, x1, q4, q5, q6, q7);
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = tid; i < N; i += NT) g[i] = s[i];
+}
+
+// ---------------------------------------------------------------- half exchange
+//
+// One rank's side of the pairwise exchange, transfer fused with the update:
+// `theirs` is the partner slice mapped through CUDA IPC, so a[j] of the
+// partner is a 16-B NVLink load and the returned element a 16-B NVLink store.
+// Every CTA streams its own chunk; thousands of CTAs in flight overlap the
+// remote traffic with the local read/update/write (the paper's T = max(Tcomp,
+// Tcomm) pipeline, distributed.py:205-290, without staging buffers).
+
+__global__ void __launch_bounds__(BLK) k_exchange(double2 *__restrict__ mine, double2 *__restrict__ theirs,
+                                                  uint64_t count, uint64_t base, int c_local, int own_is_zero,
+                                                  GateQ q) {
+  const uint64_t p0 = (uint64_t)blockIdx.x * (BLK * UNROLL) + threadIdx.x;
+  double2 am[UNROLL], at[UNROLL];
+  uint64_t jj[UNROLL];
+#pragma unroll
+  for (int u = 0; u < UNROLL; ++u) {
+    const uint64_t p = p0 + (uint64_t)u * BLK;
+    jj[u] = base + (c_local >= 0 ? insert_one(p, c_local) : p);
+    if (p < count) {
+      am[u] = mine[jj[u]];
+      at[u] = theirs[jj[u]];
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < UNROLL; ++u) {
+    const uint64_t p = p0 + (uint64_t)u * BLK;
+    if (p >= count) continue;
+    double2 keep, ret;
+    if (own_is_zero) {  // a0 = mine, a1 = theirs
+      keep = mix(am[u], at[u], q.v[0], q.v[1], q.v[2], q.v[3]);
+      ret = mix(am[u], at[u], q.v[4], q.v[5], q.v[6], q.v[7]);
+    } else {  // a0 = theirs, a1 = mine
+      keep = mix(at[u], am[u], q.v[4], q.v[5], q.v[6], q.v[7]);
+      ret = mix(at[u], am[u], q.v[0], q.v[1], q.v[2], q.v[3]);
+    }
+    mine[jj[u]] = keep;
+    theirs[jj[u]] = ret;
+  }
+  // Make the remote stores globally performed before the grid retires, so the
+  // stream-ordered fence that follows publishes them to the partner.
+  __threadfence_system();
+}
+
+// ------------------------------------------------------------ register helpers
+
+constexpr int NORM_BLOCKS = SV_NORM_SCRATCH - 1;  // 1024
+
+__global__ void __launch_bounds__(BLK) k_norm_partial(const double2 *__restrict__ a, uint64_t n, int qubit,
+                                                      double *__restrict__ partial) {
+  __shared__ double red[BLK];
+  double acc = 0.0;
+  const uint64_t stride = (uint64_t)NORM_BLOCKS * BLK;
+  for (uint64_t i = (uint64_t)blockIdx.x * BLK + threadIdx.x; i < n; i += stride) {
+    if (qubit >= 0 && !((i >> qubit) & 1ull)) continue;
+    const double2 v = a[i];
+    acc = __fma_rn(v.x, v.x, acc);
+    acc = __fma_rn(v.y, v.y, acc);
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = BLK / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
+}
+
+__global__ void __launch_bounds__(BLK) k_norm_final(double *__restrict__ partial) {
+  __shared__ double red[BLK];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < NORM_BLOCKS; i += BLK) acc += partial[i];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = BLK / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[NORM_BLOCKS] = red[0];
+}
+
+// Philox4x32-10 (Salmon et al., SC'11), counter = global amplitude index.
+__device__ __forceinline__ uint4 philox(uint4 ctr, uint2 key) {
+  const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u, W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t hi0 = __umulhi(M0, ctr.x), lo0 = M0 * ctr.x;
+    const uint32_t hi1 = __umulhi(M1, ctr.z), lo1 = M1 * ctr.z;
+    ctr = make_uint4(hi1 ^ ctr.y ^ key.x, lo1, hi0 ^ ctr.w ^ key.y, lo0);
+    key.x += W0;
+    key.y += W1;
+  }
+  return ctr;
+}
+
+__global__ void __launch_bounds__(BLK) k_init_random(double2 *__restrict__ a, uint64_t n, uint64_t gbase,
+                                                     uint64_t seed) {
+  const uint64_t i = (uint64_t)blockIdx.x * BLK + threadIdx.x;
+  if (i >= n) return;
+  const uint64_t g = gbase + i;
+  const uint4 r = philox(make_uint4((uint32_t)g, (uint32_t)(g >> 32), 0x51u, 0x7u),
+                         make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
+  const uint64_t b1 = ((uint64_t)r.x << 32) | r.y, b2 = ((uint64_t)r.z << 32) | r.w;
+  const double u1 = ((double)(b1 >> 11) + 1.0) * 0x1.0p-53;  // (0, 1]
+  const double u2 = (double)(b2 >> 11) * 0x1.0p-53;          // [0, 1)
+  const double rad = sqrt(-2.0 * log(u1));
+  double sn, cs;
+  sincospi(2.0 * u2, &sn, &cs);
+  a[i] = make_double2(rad * cs, rad * sn);
+}
+
+__global__ void __launch_bounds__(BLK) k_scale(double2 *__restrict__ a, uint64_t n, double s) {
+  for (uint64_t i = (uint64_t)blockIdx.x * BLK + threadIdx.x; i < n; i += (uint64_t)gridDim.x * BLK) {
+    const double2 v = a[i];
+    a[i] = make_double2(v.x * s, v.y * s);
+  }
+}
+
+__global__ void __launch_bounds__(BLK) k_basis(double2 *__restrict__ a, uint64_t n, int64_t local) {
+  for (uint64_t i = (uint64_t)blockIdx.x * BLK + threadIdx.x; i < n; i += (uint64_t)gridDim.x * BLK)
+    a[i] = make_double2((int64_t)i == local ? 1.0 : 0.0, 0.0);
+}
+
+// ------------------------------------------------------------------ host side
+
+bool bad_ptr(const void *p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15u) != 0; }
+
+unsigned grid_for(uint64_t items, uint64_t per_block) {
+  return (unsigned)((items + per_block - 1) / per_block);
+}
+
+unsigned fill_grid(uint64_t n) {
+  uint64_t g = (n + BLK - 1) / BLK;
+  const uint64_t cap = 148ull * 16;
+  return (unsigned)(g < cap ? (g ? g : 1) : cap);
+}
+
+// Launch a single-qubit update on (virtual) target tv of an index space of
+// 2^vbits elements; the mode decides the address map.
+template <int MODE>
+int launch_local(double2 *a, int vbits, int tv, int c, const GateQ &q, cudaStream_t st, const char *what) {
+  const uint64_t nvirt = 1ull << vbits;
+  if (vbits >= 5 && tv < 5) {
+    k_shfl<MODE><<<grid_for(nvirt, BLK * UNROLL), BLK, 0, st>>>(a, nvirt, tv, c, q);
+  } else {
+    const uint64_t np = nvirt >> 1;
+    k_pairs<MODE><<<grid_for(np, BLK * UNROLL), BLK, 0, st>>>(a, np, tv, c, q);
+  }
+  return after_launch(what);
+}
+
+template <int T>
+int launch_fused_t(double2 *a, int m, const FusedParams &P, cudaStream_t st) {
+  const size_t smem = sizeof(double2) << T;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_fused<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return fail(SV_ECUDA, "sv_apply_fused: smem attribute: %s", cudaGetErrorString(e));
+  }
+  const uint64_t nblocks = 1ull << (m - T);
+  k_fused<T><<<(unsigned)nblocks, FusedShape<T>::NT, smem, st>>>(a, P);
+  return after_launch("sv_apply_fused");
+}
+
+int launch_fused(double2 *a, int m, int T, const FusedParams &P, cudaStream_t st) {
+  switch (T) {
+    case 1: return launch_fused_t<1>(a, m, P, st);
+    case 2: return launch_fused_t<2>(a, m, P, st);
+    case 3: return launch_fused_t<3>(a, m, P, st);
+    case 4: return launch_fused_t<4>(a, m, P, st);
+    case 5: return launch_fused_t<5>(a, m, P, st);
+    case 6: return launch_fused_t<6>(a, m, P, st);
+    case 7: return launch_fused_t<7>(a, m, P, st);
+    case 8: return launch_fused_t<8>(a, m, P, st);
+    case 9: return launch_fused_t<9>(a, m, P, st);
+    case 10: return launch_fused_t<10>(a, m, P, st);
+    case 11: return launch_fused_t<11>(a, m, P, st);
+    case 12: return launch_fused_t<12>(a, m, P, st);
+    case 13: return launch_fused_t<13>(a, m, P, st);
+    default: return fail(SV_EINVAL, "sv_apply_fused: tile exponent %d unsupported", T);
+  }
+}
+
+typedef CUresult (*PFN_getAddressRange)(CUdeviceptr *, size_t *, CUdeviceptr);
+
+int alloc_base(const void *ptr, uintptr_t *base) {
+  static PFN_getAddressRange fn = nullptr;
+  if (!fn) {
+    void *f = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    cudaError_t e = cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &qr);
+    if (e != cudaSuccess || qr != cudaDriverEntryPointSuccess || !f)
+      return fail(SV_ECUDA, "sv_ipc_handle: cuMemGetAddressRange unavailable");
+    fn = (PFN_getAddressRange)f;
+  }
+  CUdeviceptr b = 0;
+  size_t sz = 0;
+  CUresult r = fn(&b, &sz, (CUdeviceptr)(uintptr_t)ptr);
+  if (r != CUDA_SUCCESS) return fail(SV_ECUDA, "sv_ipc_handle: address range lookup failed (%d)", (int)r);
+  *base = (uintptr_t)b;
+  return SV_OK;
+}
+
+}  // namespace
+
+// ======================================================================= C ABI
+
+extern "C" {
+
+int sv_version(void) { return SV_ABI_VERSION; }
+
+const char *sv_last_error(void) { return g_err; }
+
+uint64_t sv_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+int sv_apply_single(void *amps, int m, int k, const double *q, void *stream) {
+  if (bad_ptr(amps) || !q) return fail(SV_EINVAL, "sv_apply_single: null or misaligned pointer");
+  if (m < 1 || m > 62) return fail(SV_EINVAL, "sv_apply_single: m=%d out of range", m);
+  if (k < 0 || k >= m) return fail(SV_EINVAL, "sv_apply_single: qubit %d not in [0, %d)", k, m);
+  return launch_local<MODE_SINGLE>((double2 *)amps, m, k, 0, load_q(q), (cudaStream_t)stream,
+                                   "sv_apply_single");
+}
+
+int sv_apply_controlled(void *amps, int m, int c, int t, const double *q, void *stream) {
+  if (bad_ptr(amps) || !q) return fail(SV_EINVAL, "sv_apply_controlled: null or misaligned pointer");
+  if (m < 2 || m > 62) return fail(SV_EINVAL, "sv_apply_controlled: m=%d out of range", m);
+  if (c == t) return fail(SV_EINVAL, "sv_apply_controlled: control and target must differ, both are %d", c);
+  if (c < 0 || c >= m || t < 0 || t >= m)
+    return fail(SV_EINVAL, "sv_apply_controlled: qubits (%d,%d) not in [0, %d)", c, t, m);
+  const GateQ g = load_q(q);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (c == 0) return launch_local<MODE_PRED>((double2 *)amps, m, t, 0, g, st, "sv_apply_controlled");
+  const int tv = t < c ? t : t - 1;
+  return launch_local<MODE_CTL>((double2 *)amps, m - 1, tv, c, g, st, "sv_apply_controlled");
+}
+
+int sv_apply_fused(void *amps, int m, int l, const sv_gate *gates, int ngates, void *stream) {
+  if (bad_ptr(amps) || !gates) return fail(SV_EINVAL, "sv_apply_fused: null or misaligned pointer");
+  if (m < 1 || m > 62) return fail(SV_EINVAL, "sv_apply_fused: m=%d out of range", m);
+  const int lmax = m < SV_FUSED_MAX_TILE ? m : SV_FUSED_MAX_TILE;
+  if (l < 1 || l > lmax) return fail(SV_EINVAL, "sv_apply_fused: block exponent %d not in [1, %d]", l, lmax);
+  if (ngates < 1 || ngates > SV_FUSED_MAX_GATES)
+    return fail(SV_EINVAL, "sv_apply_fused: %d gates not in [1, %d]", ngates, SV_FUSED_MAX_GATES);
+  static thread_local FusedParams P;  // 18 KB: keep it off the stack
+  P.ngates = ngates;
+  P.pad = 0;
+  for (int i = 0; i < ngates; ++i) {
+    const sv_gate &g = gates[i];
+    if (g.target < 0 || g.target >= l || g.control >= l || g.control < -1 || g.control == g.target)
+      return fail(SV_EINVAL, "sv_apply_fused: gate %d (t=%d, c=%d) outside block exponent %d", i, g.target,
+                  g.control, l);
+    P.g[i] = g;
+  }
+  // Tile: at least 2^12 amplitudes per CTA where the slice allows (occupancy:
+  // 64 KiB tiles give 3 CTAs/SM), never below the block exponent.
+  int T = l > 12 ? l : (m < 12 ? m : 12);
+  return launch_fused((double2 *)amps, m, T, P, (cudaStream_t)stream);
+}
+
+int sv_exchange(void *mine, void *theirs, int m, int own_is_zero, int c_local, const double *q, void *stream) {
+  if (bad_ptr(mine) || bad_ptr(theirs) || !q) return fail(SV_EINVAL, "sv_exchange: null or misaligned pointer");
+  if (mine == theirs) return fail(SV_EINVAL, "sv_exchange: partner slice aliases the local slice");
+  if (m < 1 || m > 62) return fail(SV_EINVAL, "sv_exchange: m=%d out of range", m);
+  if (c_local < -1 || c_local >= m) return fail(SV_EINVAL, "sv_exchange: control %d not local (m=%d)", c_local, m);
+  const uint64_t half = 1ull << (m - 1);
+  const uint64_t base = own_is_zero ? 0 : half;
+  uint64_t count;
+  int cmap = c_local;
+  if (c_local < 0) {
+    count = half;
+  } else if (c_local == m - 1) {  // the half-selecting bit: all of the second half, none of the first
+    count = own_is_zero ? 0 : half;
+    cmap = -1;
+  } else {
+    count = half >> 1;
+  }
+  if (count == 0) return SV_OK;
+  k_exchange<<<grid_for(count, BLK * UNROLL), BLK, 0, (cudaStream_t)stream>>>(
+      (double2 *)mine, (double2 *)theirs, count, base, cmap, own_is_zero ? 1 : 0, load_q(q));
+  return after_launch("sv_exchange");
+}
+
+int sv_norm_sq(const void *amps, int m, int qubit, double *scratch, void *stream) {
+  if (bad_ptr(amps) || !scratch) return fail(SV_EINVAL, "sv_norm_sq: null or misaligned pointer");
+  if (m < 0 || m > 62) return fail(SV_EINVAL, "sv_norm_sq: m=%d out of range", m);
+  if (qubit < -1 || qubit >= m) return fail(SV_EINVAL, "sv_norm_sq: qubit %d not local (m=%d)", qubit, m);
+  cudaStream_t st = (cudaStream_t)stream;
+  k_norm_partial<<<NORM_BLOCKS, BLK, 0, st>>>((const double2 *)amps, 1ull << m, qubit, scratch);
+  k_norm_final<<<1, BLK, 0, st>>>(scratch);
+  return after_launch("sv_norm_sq", 2);
+}
+
+int sv_init_random(void *amps, int m, uint64_t seed, uint64_t rank, void *stream) {
+  if (bad_ptr(amps)) return fail(SV_EINVAL, "sv_init_random: null or misaligned pointer");
+  if (m < 0 || m > 62) return fail(SV_EINVAL, "sv_init_random: m=%d out of range", m);
+  const uint64_t n = 1ull << m;
+  k_init_random<<<grid_for(n, BLK), BLK, 0, (cudaStream_t)stream>>>((double2 *)amps, n, rank << m, seed);
+  return after_launch("sv_init_random");
+}
+
+int sv_scale(void *amps, int m, double s, void *stream) {
+  if (bad_ptr(amps)) return fail(SV_EINVAL, "sv_scale: null or misaligned pointer");
+  if (m < 0 || m > 62) return fail(SV_EINVAL, "sv_scale: m=%d out of range", m);
+  const uint64_t n = 1ull << m;
+  k_scale<<<fill_grid(n), BLK, 0, (cudaStream_t)stream>>>((double2 *)amps, n, s);
+  return after_launch("sv_scale");
+}
+
+int sv_init_basis(void *amps, int m, int64_t local, void *stream) {
+  if (bad_ptr(amps)) return fail(SV_EINVAL, "sv_init_basis: null or misaligned pointer");
+  if (m < 0 || m > 62) return fail(SV_EINVAL, "sv_init_basis: m=%d out of range", m);
+  const uint64_t n = 1ull << m;
+  if (local >= (int64_t)n) return fail(SV_EINVAL, "sv_init_basis: index %lld outside slice", (long long)local);
+  k_basis<<<fill_grid(n), BLK, 0, (cudaStream_t)stream>>>((double2 *)amps, n, local);
+  return after_launch("sv_init_basis");
+}
+
+int sv_copy(void *dst, const void *src, uint64_t nbytes, void *stream) {
+  if (!dst || !src) return fail(SV_EINVAL, "sv_copy: null pointer");
+  cudaError_t e = cudaMemcpyAsync(dst, src, (size_t)nbytes, cudaMemcpyDefault, (cudaStream_t)stream);
+  if (e != cudaSuccess) return fail(SV_ECUDA, "sv_copy: %s", cudaGetErrorString(e));
+  return SV_OK;
+}
+
+int sv_ipc_handle(const void *ptr, void *handle_out, uint64_t *offset_out) {
+  if (!ptr || !handle_out || !offset_out) return fail(SV_EINVAL, "sv_ipc_handle: null argument");
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  uintptr_t base = 0;
+  int rc = alloc_base(ptr, &base);
+  if (rc != SV_OK) return rc;
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, (void *)base);
+  if (e != cudaSuccess) return fail(SV_ECUDA, "sv_ipc_handle: %s", cudaGetErrorString(e));
+  memcpy(handle_out, &h, sizeof(h));
+  *offset_out = (uint64_t)((uintptr_t)ptr - base);
+  return SV_OK;
+}
+
+int sv_ipc_open(const void *handle, uint64_t offset, void **ptr_out) {
+  if (!handle || !ptr_out) return fail(SV_EINVAL, "sv_ipc_open: null argument");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  void *p = nullptr;
+  cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return fail(SV_ECUDA, "sv_ipc_open: %s", cudaGetErrorString(e));
+  *ptr_out = (void *)((uintptr_t)p + offset);
+  return SV_OK;
+}
+
+int sv_ipc_close(void *ptr, uint64_t offset) {
+  if (!ptr) return fail(SV_EINVAL, "sv_ipc_close: null pointer");
+  cudaError_t e = cudaIpcCloseMemHandle((void *)((uintptr_t)ptr - offset));
+  if (e != cudaSuccess) return fail(SV_ECUDA, "sv_ipc_close: %s", cudaGetErrorString(e));
+  return SV_OK;
+}
+
+}  // extern "C"

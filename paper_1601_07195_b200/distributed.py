@@ -1,0 +1,486 @@
+"""Gates on global qubits: pairwise NVLink exchange (mirror of pkg/src/svsim/distributed.py).
+
+Rank r holds global indices [r*2^m, (r+1)*2^m).  A gate on qubit k >= m pairs
+local element j of rank r with local element j of partner r ^ 2^(k-m)
+(distributed.py:1-15).  The reference streams halves through a byte
+transport in double-buffered chunks; here the data plane is the partner's
+slice itself, mapped into this process with CUDA IPC, and the whole half
+exchange is ONE kernel (``sv_exchange``): the zero side updates the first
+half of every pair, the one side the second half, each reading the partner's
+element over NVLink and storing the returned element straight back into the
+partner's HBM.  Thousands of CTAs in flight overlap transfer and update, the
+paper's T = max(T_comp, T_comm) pipeline (distributed.py:205-290) without
+staging buffers or per-chunk host work.
+
+Control plane (host): ``NvlinkFabric`` replaces the Transport ABC
+(distributed.py:60-92).  It owns the process group, the IPC peer mappings,
+the per-gate fences and the byte counters of ``CountingTransport``
+(transport.py:549-598).  Fences are stream-ordered NCCL all-reduces of one
+int (no host sync) when the group runs NCCL, host barriers otherwise.
+
+Host logic is split from execution: ``plan_gate`` is the pure per-rank
+decision of distributed.py:353-459 (which kernel, which partner, which half,
+how many bytes), ``execute_action`` runs it against a device executor.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import enum
+import threading
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .core import AMP_BYTES, LocalState
+from .errors import LayoutError, TransportError
+from .kernels import (
+    SERIAL,
+    GateMatrix,
+    ThreadPolicy,
+    _as_gate,
+    apply_controlled_raw,
+    apply_single_raw,
+    device_view,
+    stream_handle,
+)
+from .perfmodel import BoundCase, classify_case
+
+DEFAULT_CHUNK_BYTES = 4 << 20
+GATHER_MAX_QUBITS = 26
+CONTROL_TAG = 0
+
+
+class ComputesHalf(enum.Enum):
+    FIRST_HALF = 0
+    SECOND_HALF = 1
+
+
+@dataclass(frozen=True)
+class ExchangePlan:
+    """Who faces whom for one exchange, and the (API-compatible) chunking (distributed.py:100-122).
+
+    The fused NVLink kernel has no staging buffers; chunk_amps / temp_capacity
+    are validated exactly like the reference and otherwise only affect nothing:
+    results are bitwise independent of them, as the reference guarantees.
+    """
+
+    partner: int
+    this_rank_computes: ComputesHalf
+    chunk_amps: int
+    temp_capacity: int
+    half_amps: int
+
+    def __post_init__(self):
+        if self.chunk_amps < 1:
+            raise ValueError("chunk_amps must be >= 1")
+        if self.half_amps % self.chunk_amps != 0:
+            raise ValueError(f"chunk_amps {self.chunk_amps} must divide the half length {self.half_amps}")
+        steps = self.half_amps // self.chunk_amps
+        needed = self.chunk_amps * min(2, steps)
+        if not needed <= self.temp_capacity <= self.half_amps:
+            raise ValueError(f"temp_capacity {self.temp_capacity} outside [{needed}, {self.half_amps}]")
+
+
+def make_exchange_plan(layout, k: int, *, chunk_amps: int | None = None, chunk_bytes: int | None = None,
+                       temp_capacity: int | None = None) -> ExchangePlan:
+    """Plan for pairing bit k >= m (distributed.py:125-158)."""
+    m = layout.m
+    if not m <= k < layout.n:
+        raise LayoutError(f"qubit {k} is local (m={m}); no exchange needed")
+    half = 1 << (m - 1)
+    if chunk_amps is None:
+        want = max(1, (chunk_bytes or DEFAULT_CHUNK_BYTES) // AMP_BYTES)
+        chunk_amps = min(1 << (want.bit_length() - 1), half)
+    steps = max(1, half // max(1, chunk_amps))
+    if temp_capacity is None:
+        temp_capacity = chunk_amps * min(2, steps)
+    zero_side = ((layout.rank >> (k - m)) & 1) == 0
+    return ExchangePlan(
+        partner=layout.rank ^ (1 << (k - m)),
+        this_rank_computes=ComputesHalf.FIRST_HALF if zero_side else ComputesHalf.SECOND_HALF,
+        chunk_amps=chunk_amps,
+        temp_capacity=temp_capacity,
+        half_amps=half,
+    )
+
+
+class ScratchPool:
+    """API-compatible scratch accounting (distributed.py:161-181).
+
+    The fused exchange stages nothing, so the pool is never drawn from by the
+    gate path and ``high_water_bytes`` stays 0; take/give keep working for
+    callers that use it directly.
+    """
+
+    def __init__(self):
+        self._free: dict[int, list[torch.Tensor]] = {}
+        self._lock = threading.Lock()
+        self.outstanding_bytes = 0
+        self.high_water_bytes = 0
+
+    def take(self, num_amps: int, device=None) -> torch.Tensor:
+        with self._lock:
+            stack = self._free.get(num_amps)
+            buf = stack.pop() if stack else torch.zeros(
+                num_amps, dtype=torch.complex128,
+                device=device if device is not None else torch.device("cuda", torch.cuda.current_device()))
+            self.outstanding_bytes += num_amps * AMP_BYTES
+            self.high_water_bytes = max(self.high_water_bytes, self.outstanding_bytes)
+            return buf
+
+    def give(self, buf: torch.Tensor) -> None:
+        with self._lock:
+            self._free.setdefault(buf.shape[0], []).append(buf)
+            self.outstanding_bytes -= buf.shape[0] * AMP_BYTES
+
+
+# ------------------------------------------------------------------ host logic
+
+
+@dataclass(frozen=True)
+class GateAction:
+    """What one rank does for one gate (pure function of layout and gate)."""
+
+    kind: str            # "single" | "controlled" | "exchange" | "idle" (local no-op) | "idle_exchange"
+    case: BoundCase
+    target: int
+    control: int | None
+    partner: int = -1
+    own_is_zero: bool = True
+    c_local: int = -1    # >= 0: only local-bit-c elements cross (case 5)
+    sent: int = 0        # payload bytes leaving this rank over NVLink
+    received: int = 0
+
+    @property
+    def fenced(self) -> bool:
+        """Every rank fences around cases 2/5/6 (participating or not)."""
+        return self.kind in ("exchange", "idle_exchange")
+
+
+def plan_gate(layout, target: int, control: int | None) -> GateAction:
+    """Per-rank routing of distributed.py:314-459 (cases of perfmodel.py:30-38)."""
+    m, rank = layout.m, layout.rank
+    case = classify_case(target, control, m)
+    if control is None:
+        if target < m:
+            return GateAction("single", case, target, None)
+        bit = target - m
+        return GateAction("exchange", case, target, None, partner=rank ^ (1 << bit),
+                          own_is_zero=((rank >> bit) & 1) == 0, sent=1 << (m + 4), received=1 << (m + 4))
+    c, t = control, target
+    if c < m and t < m:
+        return GateAction("controlled", case, t, c)
+    if t < m:  # case 4: control in the rank bits, target local
+        on = (rank >> (c - m)) & 1
+        return GateAction("single" if on else "idle", case, t, c)
+    bit = t - m
+    partner = rank ^ (1 << bit)
+    zero = ((rank >> bit) & 1) == 0
+    if c >= m:  # case 6: only control-set ranks exchange
+        if (rank >> (c - m)) & 1:
+            return GateAction("exchange", case, t, c, partner=partner, own_is_zero=zero,
+                              sent=1 << (m + 4), received=1 << (m + 4))
+        return GateAction("idle_exchange", case, t, c)
+    # case 5: local control, remote target -- packed bit-c = 1 elements
+    return GateAction("exchange", case, t, c, partner=partner, own_is_zero=zero, c_local=c,
+                      sent=1 << (m + 3), received=1 << (m + 3))
+
+
+# ------------------------------------------------------------ device executor
+
+
+class CudaExecutor:
+    """libsvb200 launches on the current stream (the only product executor)."""
+
+    def single(self, state: LocalState, k: int, q: GateMatrix) -> None:
+        apply_single_raw(state.amps, k, q)
+
+    def controlled(self, state: LocalState, c: int, t: int, q: GateMatrix) -> None:
+        apply_controlled_raw(state.amps, c, t, q)
+
+    def exchange(self, state: LocalState, theirs: int, own_is_zero: bool, c_local: int, q: GateMatrix) -> None:
+        ptr, m = device_view(state.amps)
+        with torch.cuda.device(state.amps.device):
+            _lib.check(_lib.load().sv_exchange(ptr, theirs, m, int(own_is_zero), int(c_local),
+                                               _as_gate(q).qbuf(), stream_handle()))
+
+    def synchronize(self, state: LocalState) -> None:
+        torch.cuda.current_stream(state.amps.device).synchronize()
+
+    def key(self, state: LocalState) -> tuple:
+        return (state.amps.data_ptr(), state.amps.numel(), str(state.amps.device))
+
+    def flag_device(self, state: LocalState | None) -> torch.device:
+        return state.amps.device if state is not None else torch.device("cuda", torch.cuda.current_device())
+
+    def share(self, state: LocalState):
+        """(64-byte IPC handle, byte offset) of the slice's allocation."""
+        h = (ctypes.c_char * 64)()
+        off = ctypes.c_uint64(0)
+        with torch.cuda.device(state.amps.device):
+            _lib.check(_lib.load().sv_ipc_handle(state.amps.data_ptr(), h, ctypes.byref(off)))
+        return bytes(h), int(off.value)
+
+    def open(self, state: LocalState, blob) -> int:
+        handle, off = blob
+        p = ctypes.c_void_p()
+        with torch.cuda.device(state.amps.device):
+            _lib.check(_lib.load().sv_ipc_open(ctypes.c_char_p(handle), off, ctypes.byref(p)))
+        return int(p.value)
+
+    def close(self, ptr: int, blob) -> None:
+        _lib.check(_lib.load().sv_ipc_close(ptr, blob[1]))
+
+    def copy(self, dst: int, src: int, nbytes: int, state: LocalState) -> None:
+        with torch.cuda.device(state.amps.device):
+            _lib.check(_lib.load().sv_copy(dst, src, nbytes, stream_handle()))
+
+
+_CUDA = CudaExecutor()
+
+
+class NvlinkFabric:
+    """Exchange fabric over one torch.distributed group, one rank per GPU.
+
+    Stands in for the reference's ``transport`` argument everywhere
+    (apply_op, run_circuit, global_norm_sq, gather_full_state).  Counters
+    follow CountingTransport: payload bytes sent / received over the link.
+    """
+
+    def __init__(self, group=None, *, fence: str | None = None, executor=None):
+        import torch.distributed as dist
+
+        if not dist.is_initialized():
+            raise TransportError("NvlinkFabric needs an initialised torch.distributed process group")
+        self._dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.num_ranks = dist.get_world_size(group)
+        backend = str(dist.get_backend(group)).lower()
+        self.fence_mode = fence or ("stream" if backend == "nccl" else "host")
+        if self.fence_mode not in ("stream", "host"):
+            raise ValueError("fence must be 'stream' or 'host'")
+        self.executor = executor or _CUDA
+        self.sent_bytes = 0
+        self.received_bytes = 0
+        self.fences = 0
+        self._tag = CONTROL_TAG
+        self._lock = threading.Lock()
+        self._peers: dict[tuple, tuple[list, list]] = {}
+        self._flag: torch.Tensor | None = None
+
+    # --- Transport-compatible surface
+    def fresh_tag(self) -> int:
+        self._tag += 1
+        return self._tag
+
+    def snapshot(self) -> tuple[int, int]:
+        with self._lock:
+            return self.sent_bytes, self.received_bytes
+
+    @property
+    def total_bytes(self) -> int:
+        return self.sent_bytes + self.received_bytes
+
+    def count(self, sent: int, received: int) -> None:
+        with self._lock:
+            self.sent_bytes += sent
+            self.received_bytes += received
+
+    def exchange_objects(self, obj) -> list:
+        out = [None] * self.num_ranks
+        self._dist.all_gather_object(out, obj, group=self.group)
+        return out
+
+    def reduce_sum(self, partial: float) -> float:
+        """Rank-ordered sum (deterministic, identical on every rank)."""
+        total = 0.0
+        for v in self.exchange_objects(float(partial)):
+            total += v
+        return total
+
+    def barrier(self, state: LocalState | None = None) -> None:
+        self.fences += 1
+        if self.fence_mode == "stream":
+            dev = self.executor.flag_device(state)
+            if self._flag is None or self._flag.device != dev:
+                self._flag = torch.zeros(1, dtype=torch.int32, device=dev)
+            self._dist.all_reduce(self._flag, group=self.group)
+        else:
+            if state is not None:
+                self.executor.synchronize(state)
+            self._dist.barrier(group=self.group)
+
+    # --- peer mappings
+    def ensure_registered(self, state: LocalState) -> None:
+        """Collective: map every rank's slice into this process (once per slice)."""
+        key = self.executor.key(state)
+        if key in self._peers:
+            return
+        blobs = self.exchange_objects(self.executor.share(state))
+        ptrs = [None] * self.num_ranks
+        for r, blob in enumerate(blobs):
+            if r != self.rank:
+                ptrs[r] = self.executor.open(state, blob)
+        self._peers[key] = (ptrs, blobs)
+
+    def peer_pointer(self, state: LocalState, rank: int) -> int:
+        key = self.executor.key(state)
+        try:
+            ptr = self._peers[key][0][rank]
+        except KeyError as exc:
+            raise TransportError("slice not registered with the fabric") from exc
+        if ptr is None:
+            raise TransportError(f"rank {rank} is this rank; no peer mapping")
+        return ptr
+
+    def release(self, state: LocalState) -> None:
+        """Unmap the peers' slices registered for `state` (collective-free)."""
+        entry = self._peers.pop(self.executor.key(state), None)
+        if entry:
+            for ptr, blob in zip(*entry):
+                if ptr is not None:
+                    self.executor.close(ptr, blob)
+
+    def close(self) -> None:
+        for key in list(self._peers):
+            ptrs, blobs = self._peers.pop(key)
+            for ptr, blob in zip(ptrs, blobs):
+                if ptr is not None:
+                    try:
+                        self.executor.close(ptr, blob)
+                    except Exception:
+                        pass
+
+
+def execute_action(state: LocalState, action: GateAction, q: GateMatrix, fabric: NvlinkFabric | None,
+                   executor=None) -> None:
+    """Run one rank's share of one gate; fences bracket every exchange-class gate on all ranks."""
+    ex = executor or (fabric.executor if fabric is not None else _CUDA)
+    if action.kind == "single":
+        ex.single(state, action.target, q)
+    elif action.kind == "controlled":
+        ex.controlled(state, action.control, action.target, q)
+    if not action.fenced:
+        return
+    if fabric is None:
+        raise LayoutError(f"gate on qubit {action.target} needs a transport")
+    try:
+        # Partner slices are read and written in place: every rank's prior
+        # work must be complete before, and the exchange complete after.
+        fabric.barrier(state)
+        if action.kind == "exchange":
+            ex.exchange(state, fabric.peer_pointer(state, action.partner), action.own_is_zero, action.c_local, q)
+        fabric.count(action.sent, action.received)
+        fabric.barrier(state)
+    except BaseException:
+        state.corrupt = True
+        raise
+
+
+# ------------------------------------------------------------- reference API
+
+
+def _check_transport(transport, lay):
+    if transport is None:
+        raise LayoutError("distributed gate application needs a transport")
+    if transport.num_ranks != lay.num_ranks or transport.rank != lay.rank:
+        raise LayoutError(
+            f"fabric rank {transport.rank}/{transport.num_ranks} does not match layout "
+            f"rank {lay.rank}/{lay.num_ranks}")
+
+
+def apply_single_distributed(state: LocalState, k: int, q: GateMatrix, transport: NvlinkFabric, *,
+                             plan: ExchangePlan | None = None, chunk_amps: int | None = None,
+                             scratch: ScratchPool | None = None, policy: ThreadPolicy = SERIAL) -> None:
+    """Single-qubit gate on global qubit k >= m via the fused half exchange (distributed.py:314-338)."""
+    lay = state.layout
+    if lay.p < 1:
+        raise LayoutError("distributed gate application needs at least 2 ranks")
+    if not lay.m <= k < lay.n:
+        raise LayoutError(f"qubit {k} is local (m={lay.m}); use the local kernel")
+    _check_transport(transport, lay)
+    transport.fresh_tag()
+    if plan is None:
+        plan = make_exchange_plan(lay, k, chunk_amps=chunk_amps)
+    action = plan_gate(lay, k, None)
+    if plan.partner != action.partner or (plan.this_rank_computes is ComputesHalf.FIRST_HALF) != action.own_is_zero:
+        raise TransportError("exchange plan does not match this rank's pairing")
+    transport.ensure_registered(state)
+    execute_action(state, action, _as_gate(q), transport)
+
+
+def apply_controlled_distributed(state: LocalState, c: int, t: int, q: GateMatrix, transport: NvlinkFabric, *,
+                                 plan: ExchangePlan | None = None, chunk_amps: int | None = None,
+                                 scratch: ScratchPool | None = None, policy: ThreadPolicy = SERIAL) -> None:
+    """Controlled gate with a qubit in the rank bits: cases 4, 5, 6 (distributed.py:353-422)."""
+    lay = state.layout
+    if c == t:
+        raise ValueError(f"control and target must differ, both are {c}")
+    if not (0 <= c < lay.n and 0 <= t < lay.n):
+        raise ValueError(f"qubits ({c},{t}) out of range for n={lay.n}")
+    if lay.p < 1:
+        raise LayoutError("distributed gate application needs at least 2 ranks")
+    m = lay.m
+    if c < m and t < m:
+        apply_controlled_raw(state.amps, c, t, q, policy)
+        return
+    _check_transport(transport, lay)
+    transport.fresh_tag()
+    if t >= m and plan is None:
+        plan = make_exchange_plan(lay, t, chunk_amps=chunk_amps)
+    transport.ensure_registered(state)
+    execute_action(state, plan_gate(lay, t, c), _as_gate(q), transport)
+
+
+def apply_op(state: LocalState, op, transport: NvlinkFabric | None = None, *, policy: ThreadPolicy = SERIAL,
+             chunk_amps: int | None = None, scratch: ScratchPool | None = None) -> None:
+    """Route one GateOp to the local kernel or the exchange (distributed.py:425-459)."""
+    from .kernels import apply_controlled_local, apply_single_local
+
+    m = state.layout.m
+    if op.control is None:
+        if op.target < m:
+            apply_single_local(state, op.target, op.gate, policy)
+            return
+        if transport is None:
+            raise LayoutError(f"gate on qubit {op.target} >= m={m} requires a transport")
+        apply_single_distributed(state, op.target, op.gate, transport, chunk_amps=chunk_amps, scratch=scratch,
+                                 policy=policy)
+        return
+    if op.control < m and op.target < m:
+        apply_controlled_local(state, op.control, op.target, op.gate, policy)
+        return
+    if transport is None:
+        raise LayoutError(f"gate on qubits ({op.control},{op.target}) crosses m={m}; requires a transport")
+    apply_controlled_distributed(state, op.control, op.target, op.gate, transport, chunk_amps=chunk_amps,
+                                 scratch=scratch, policy=policy)
+
+
+def gather_full_state(state: LocalState, transport: NvlinkFabric | None = None,
+                      cap: int = GATHER_MAX_QUBITS) -> np.ndarray | None:
+    """Rank-ordered concatenation on rank 0 (None elsewhere), read over NVLink (distributed.py:462-482)."""
+    lay = state.layout
+    if lay.n > cap:
+        raise LayoutError(f"gather of 2^{lay.n} amplitudes exceeds the n <= {cap} guard")
+    if lay.p == 0:
+        return state.to_numpy()
+    if transport is None:
+        raise LayoutError("gather requires a transport when p > 0")
+    _check_transport(transport, lay)
+    transport.fresh_tag()
+    transport.ensure_registered(state)
+    transport.barrier(state)
+    full = None
+    if lay.rank == 0:
+        dev = torch.empty(1 << lay.n, dtype=torch.complex128, device=state.amps.device)
+        nbytes = lay.local_len * AMP_BYTES
+        dev[: lay.local_len].copy_(state.amps)
+        for src in range(1, lay.num_ranks):
+            transport.executor.copy(dev[src << lay.m:].data_ptr(), transport.peer_pointer(state, src), nbytes, state)
+        full = dev.cpu().numpy()
+    transport.barrier(state)
+    return full
