@@ -52,6 +52,7 @@ from .distributed import (
     NvlinkFabric,
     ScratchPool,
     apply_controlled_distributed,
+    apply_global,
     apply_op,
     apply_single_distributed,
     execute_action,

@@ -10,7 +10,7 @@
 //
 // written with __fma_rn/__dmul_rn/__dadd_rn so nvcc cannot re-associate or
 // contract differently; results are bit-identical to the reference and to
-// oracle/sv_oracle.c, and independent of launch geometry, fusion and sharding.
+// the tests' CPU oracle, and independent of launch geometry, fusion and sharding.
 
 #include <cuda.h>
 #include <cuda_runtime.h>

@@ -402,15 +402,9 @@ def apply_single_distributed(state: LocalState, k: int, q: GateMatrix, transport
         raise LayoutError("distributed gate application needs at least 2 ranks")
     if not lay.m <= k < lay.n:
         raise LayoutError(f"qubit {k} is local (m={lay.m}); use the local kernel")
-    _check_transport(transport, lay)
-    transport.fresh_tag()
     if plan is None:
         plan = make_exchange_plan(lay, k, chunk_amps=chunk_amps)
-    action = plan_gate(lay, k, None)
-    if plan.partner != action.partner or (plan.this_rank_computes is ComputesHalf.FIRST_HALF) != action.own_is_zero:
-        raise TransportError("exchange plan does not match this rank's pairing")
-    transport.ensure_registered(state)
-    execute_action(state, action, _as_gate(q), transport)
+    apply_global(state, k, None, q, transport, plan=plan)
 
 
 def apply_controlled_distributed(state: LocalState, c: int, t: int, q: GateMatrix, transport: NvlinkFabric, *,
@@ -428,12 +422,28 @@ def apply_controlled_distributed(state: LocalState, c: int, t: int, q: GateMatri
     if c < m and t < m:
         apply_controlled_raw(state.amps, c, t, q, policy)
         return
-    _check_transport(transport, lay)
-    transport.fresh_tag()
     if t >= m and plan is None:
         plan = make_exchange_plan(lay, t, chunk_amps=chunk_amps)
+    apply_global(state, t, c, q, transport, plan=plan)
+
+
+def apply_global(state, target: int, control: int | None, q, transport, *, plan: ExchangePlan | None = None,
+                 executor=None) -> None:
+    """Shared tail of the distributed entry points: one gate touching a rank bit.
+
+    Every rank calls it for every such gate (SPMD), so the collective pieces
+    -- fresh tag, slice registration, fences -- line up across ranks.
+    """
+    lay = state.layout
+    _check_transport(transport, lay)
+    transport.fresh_tag()
+    action = plan_gate(lay, target, control)
+    if plan is not None and action.kind == "exchange" and (
+            plan.partner != action.partner
+            or (plan.this_rank_computes is ComputesHalf.FIRST_HALF) != action.own_is_zero):
+        raise TransportError("exchange plan does not match this rank's pairing")
     transport.ensure_registered(state)
-    execute_action(state, plan_gate(lay, t, c), _as_gate(q), transport)
+    execute_action(state, action, _as_gate(q), transport, executor)
 
 
 def apply_op(state: LocalState, op, transport: NvlinkFabric | None = None, *, policy: ThreadPolicy = SERIAL,

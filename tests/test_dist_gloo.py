@@ -1,0 +1,159 @@
+"""Multi-rank host protocol on CPU: world_size 2/4/8 processes over gloo.
+
+The product's control plane runs for real -- NvlinkFabric (object all-gather
+for slice registration, host fences, byte counters, tags), plan_gate,
+apply_global and execute_action -- with the device swapped for a test
+executor: slices live in POSIX shared memory (standing in for IPC-mapped
+HBM) and the kernels are the oracle's C restatement (standing in for
+libsvb200).  The gathered state and every per-gate, per-rank byte count must
+equal what the reference itself produced (tests/golden/circuits_small.npz).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import socket
+import tempfile
+from dataclasses import dataclass, field
+from multiprocessing import shared_memory
+
+import numpy as np
+import pytest
+
+from conftest import unpack_ops
+
+
+@dataclass
+class ShmState:
+    layout: object
+    amps: np.ndarray
+    shm: object
+    corrupt: bool = field(default=False)
+
+
+class ShmOracleExecutor:
+    """Test double of CudaExecutor: shm 'peer mappings', oracle 'kernels'."""
+
+    def __init__(self):
+        self._open = {}
+
+    def single(self, state, k, q):
+        from oracle import oracle
+
+        oracle.apply_single(state.amps, k, q.mat)
+
+    def controlled(self, state, c, t, q):
+        from oracle import oracle
+
+        oracle.apply_controlled(state.amps, c, t, q.mat)
+
+    def exchange(self, state, theirs, own_is_zero, c_local, q):
+        from oracle import oracle
+
+        oracle.exchange_raw(state.amps.ctypes.data, theirs, state.layout.m, own_is_zero, c_local, q.mat)
+
+    def synchronize(self, state):
+        pass
+
+    def key(self, state):
+        return state.shm.name
+
+    def flag_device(self, state):
+        raise AssertionError("host fences only")
+
+    def share(self, state):
+        return (state.shm.name, 0)
+
+    def open(self, state, blob):
+        shm = shared_memory.SharedMemory(name=blob[0])
+        self._open[blob[0]] = shm
+        return ctypes.addressof(ctypes.c_char.from_buffer(shm.buf)) + blob[1]
+
+    def close(self, ptr, blob):
+        shm = self._open.pop(blob[0], None)
+        if shm is not None:
+            try:
+                shm.close()
+            except BufferError:  # ctypes view still alive; unmapped at exit
+                pass
+
+
+def _worker(rank, world, port, path, name, n):
+    import torch.distributed as dist
+
+    import paper_1601_07195_b200 as sv
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        p = world.bit_length() - 1
+        d = dict(np.load(path + ".npz"))
+        lay = sv.Layout(n, p, rank)
+        m = lay.m
+        shm = shared_memory.SharedMemory(create=True, size=16 << m, name=f"svt_{os.getpid()}_{rank}")
+        amps = np.ndarray((1 << m,), dtype=np.complex128, buffer=shm.buf)
+        amps[:] = d["init"][rank << m:(rank + 1) << m]
+        state = ShmState(lay, amps, shm)
+        ex = ShmOracleExecutor()
+        fabric = sv.NvlinkFabric(fence="host", executor=ex)
+        deltas = []
+        for t, c, q in zip(d["t"], d["c"], d["q"]):
+            t, c, gate = int(t), None if c < 0 else int(c), sv.GateMatrix.unchecked(q.reshape(2, 2))
+            before = fabric.snapshot()
+            if max(t, -1 if c is None else c) < m:
+                (ex.single(state, t, gate) if c is None else ex.controlled(state, c, t, gate))
+            else:
+                sv.apply_global(state, t, c, gate, fabric)
+            after = fabric.snapshot()
+            deltas.append((after[0] - before[0], after[1] - before[1]))
+        total = fabric.reduce_sum(float(np.sum(np.abs(amps) ** 2)))
+        blobs = fabric.exchange_objects(np.asarray(deltas, dtype=np.int64))
+        fabric.barrier()
+        if rank == 0:
+            full = np.concatenate([amps.copy()] + [
+                np.ndarray((1 << m,), dtype=np.complex128, buffer=ex._open[f"svt_{pid}_{r}"].buf).copy()
+                for r, pid in enumerate(fabric.exchange_objects(os.getpid())) if r != 0])
+        else:
+            fabric.exchange_objects(os.getpid())
+        fabric.barrier()
+        if rank == 0:
+            np.savez(path + ".out.npz", full=full, deltas=np.stack(blobs), norm=total, tags=fabric._tag,
+                     fences=fabric.fences)
+        fabric.barrier()
+        fabric.close()
+        del amps
+        shm.close()
+        shm.unlink()
+    finally:
+        dist.destroy_process_group()
+
+
+def _port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def run_world(world, name, n, golden):
+    import torch.multiprocessing as mp
+
+    d = golden("circuits_small")
+    with tempfile.TemporaryDirectory() as tmp:
+        path = os.path.join(tmp, "w")
+        np.savez(path + ".npz", init=d[f"{name}_in"], t=d[f"{name}_t"], c=d[f"{name}_c"], q=d[f"{name}_q"])
+        mp.spawn(_worker, args=(world, _port(), path, name, n), nprocs=world, join=True)
+        return dict(np.load(path + ".out.npz")), d
+
+
+@pytest.mark.parametrize("world,name,n", [(2, "mix10", 10), (4, "mix8", 8), (8, "ctl12", 12)])
+def test_gloo_world_matches_reference(golden, world, name, n):
+    out, d = run_world(world, name, n, golden)
+    p = world.bit_length() - 1
+    assert np.array_equal(out["full"], d[f"{name}_p{p}"])
+    assert np.array_equal(out["deltas"], d[f"{name}_p{p}_bytes"])
+    assert abs(float(out["norm"]) - 1.0) < 1e-12
+    m = n - p
+    glob = sum(1 for t, c, _ in unpack_ops(d, name) if max(t, -1 if c is None else c) >= m)
+    assert int(out["tags"]) == glob            # one fresh tag per global-qubit gate, on every rank
+    fenced = sum(1 for t, c, _ in unpack_ops(d, name) if t >= m)
+    assert int(out["fences"]) == 2 * fenced + 2  # two fences per exchange-class gate + two final barriers
