@@ -137,11 +137,14 @@ def load_peaks():
         return {"hbm_gbs": 6650.0}, "fallback"
 
 
-def ncu_traffic(kernel_key):
-    """dram bytes per launch of the dominant kernel from the committed ncu --set full summary."""
+def ncu_traffic(kernel_key, alg_bytes):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture
+    (profiles/ncu_summary.json), rescaled to this launch's size when the capture used a smaller
+    slice (traffic/algorithmic is size-independent once the slice is >> L2)."""
     try:
-        d = json.loads((ROOT / "profiles" / "ncu_summary.json").read_text())
-        return d["kernels"][kernel_key]["dram_bytes_per_launch"]
+        d = json.loads((ROOT / "profiles" / "ncu_summary.json").read_text())["kernels"][kernel_key]
+        scale = alg_bytes / d.get("algorithmic_bytes", alg_bytes)
+        return round(d["dram_bytes_per_launch"] * scale)
     except (OSError, KeyError, ValueError, TypeError):
         return None
 
@@ -290,7 +293,7 @@ def main():
         avg_ms = float(d.mean())
         achieved = (32 << m) / (avg_ms * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": ncu_traffic("sv_apply_single"),
+                "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": ncu_traffic("sv_apply_single", 32 << m),
                 "kernel": "k_pairs/k_shfl<MODE_SINGLE> (sv_apply_single)", "peak_kind": peak_kind,
                 "algorithmic_bytes_per_launch": 32 << m, "avg_launch_ms": round(avg_ms, 4),
                 "frac_of_8TBs": round(achieved / 8000.0, 4)}
