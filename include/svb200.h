@@ -39,6 +39,8 @@ extern "C" {
 #define SV_FUSED_MAX_TILE 13
 /* Gates carried by one fused launch (kernel parameter space). */
 #define SV_FUSED_MAX_GATES 256
+/* Gates carried by one same-target stage (sv_exchange_stage). */
+#define SV_STAGE_MAX_GATES 64
 /* Scratch doubles sv_norm_sq needs (per-block partials + result). */
 #define SV_NORM_SCRATCH 1025
 
@@ -71,6 +73,25 @@ int sv_apply_controlled(void *amps, int m, int c, int t, const double *q, void *
  * Requires 1 <= l <= min(m, SV_FUSED_MAX_TILE), every gate qubit < l,
  * 1 <= ngates <= SV_FUSED_MAX_GATES. */
 int sv_apply_fused(void *amps, int m, int l, const sv_gate *gates, int ngates, void *stream);
+
+/* Native pass planner: applies an arbitrary local gate list (targets and
+ * controls < m) in order, grouping it into as few HBM passes as the kernels
+ * allow -- maximal runs of gates with target < tile (controls anywhere: above
+ * the tile they are per-CTA predicates) go through the register-tiled kernel;
+ * maximal runs sharing one higher target go through one same-target stage
+ * pass; anything else is a single-gate launch.  Bit-identical to applying the
+ * gates one by one with sv_apply_single / sv_apply_controlled (the reference's
+ * engine.py:88-95 loop).  tile = 0 picks min(m, SV_FUSED_MAX_TILE); otherwise
+ * 9 <= tile <= min(m, SV_FUSED_MAX_TILE). */
+int sv_apply_gates(void *amps, int m, const sv_gate *gates, int ngates, int tile, void *stream);
+
+/* A stage of gates that all target the same global qubit, applied in ONE
+ * exchange (sv_exchange generalised to a gate list): each pair crosses NVLink
+ * once each way.  Controls must be local (< m) or -1; the caller drops gates
+ * whose control is a rank bit that is 0 on this rank (both partners agree).
+ * 1 <= ngates <= 64; the targets are implied by the partner pairing. */
+int sv_exchange_stage(void *mine, void *theirs, int m, int own_is_zero, const sv_gate *gates, int ngates,
+                      void *stream);
 
 /* Replaces one rank's side of the half exchange:
  * svsim.distributed._run_exchange + chunked_exchange_pipeline + _pair_kernel

@@ -19,11 +19,12 @@ SV_ECUDA = -2
 SV_FUSED_MAX_TILE = 13
 SV_FUSED_MAX_GATES = 256
 SV_NORM_SCRATCH = 1025
+SV_STAGE_MAX_GATES = 64
 ABI_VERSION = 1
 
 EXPORTS = (
     "sv_version", "sv_last_error", "sv_launch_count", "sv_apply_single", "sv_apply_controlled",
-    "sv_apply_fused", "sv_exchange", "sv_norm_sq", "sv_init_random", "sv_scale", "sv_init_basis",
+    "sv_apply_fused", "sv_apply_gates", "sv_exchange", "sv_exchange_stage","sv_norm_sq", "sv_init_random", "sv_scale", "sv_init_basis",
     "sv_copy", "sv_ipc_handle", "sv_ipc_open", "sv_ipc_close",
 )
 
@@ -61,7 +62,9 @@ def load() -> ctypes.CDLL:
         "sv_apply_single": ([vp, i, i, dp, vp], i),
         "sv_apply_controlled": ([vp, i, i, i, dp, vp], i),
         "sv_apply_fused": ([vp, i, i, ctypes.POINTER(SvGate), i, vp], i),
+        "sv_apply_gates": ([vp, i, ctypes.POINTER(SvGate), i, i, vp], i),
         "sv_exchange": ([vp, vp, i, i, i, dp, vp], i),
+        "sv_exchange_stage": ([vp, vp, i, i, ctypes.POINTER(SvGate), i, vp], i),
         "sv_norm_sq": ([vp, i, i, vp, vp], i),
         "sv_init_random": ([vp, i, u64, u64, vp], i),
         "sv_scale": ([vp, i, ctypes.c_double, vp], i),

@@ -15,6 +15,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdarg>
 #include <cstdint>
@@ -223,6 +224,236 @@ __global__ void __launch_bounds__(FusedShape<T>::NT) k_fused(double2 *__restrict
   for (int i = tid; i < N; i += NT) g[i] = s[i];
 }
 
+// ------------------------------------------------- structure-specialised pair update
+//
+// The host classifies every gate once (classify_gate):
+//   KIND_GENERAL  full mix() for both outputs (10 FP64 ops each);
+//   KIND_DIAG     q12 == q21 == 0 exactly (any zero signs):  new0 = cmul(q11,a0) + cmul(q12,a1)
+//                 where cmul(q12,a1) is a pair of signed zeros, so the add is the identity unless
+//                 a component of cmul(q11,a0) is itself zero -- only then is the second product
+//                 formed.  Bit-identical to mix(), ~40 % of its FP64 work;
+//   KIND_PHASE    KIND_DIAG with q11 == 1 + (+-0)i exactly (R_k, S, T, Z-type phases):
+//                 cmul(1,a0) == a0 whenever a0 has no zero component, so new0 is a0 untouched.
+// Zero tests are integer tests on the bit patterns (ALU pipe, not FP64).
+
+enum { KIND_GENERAL = 0, KIND_DIAG = 1, KIND_PHASE = 2 };
+
+__device__ __forceinline__ bool nonzero2(double2 v) {
+  return ((__double_as_longlong(v.x) << 1) != 0) & ((__double_as_longlong(v.y) << 1) != 0);
+}
+
+__device__ __forceinline__ double2 diag_out(double rr, double ri, double2 self, double zr, double zi,
+                                            double2 other) {
+  double2 r = cmul(rr, ri, self);
+  if (!nonzero2(r)) {
+    const double2 z = cmul(zr, zi, other);
+    r = make_double2(__dadd_rn(r.x, z.x), __dadd_rn(r.y, z.y));
+  }
+  return r;
+}
+
+template <int KIND>
+__device__ __forceinline__ void pair_update(double2 &a0, double2 &a1, const double *q) {
+  double2 n0, n1;
+  if (KIND == KIND_GENERAL) {
+    n0 = mix(a0, a1, q[0], q[1], q[2], q[3]);
+    n1 = mix(a0, a1, q[4], q[5], q[6], q[7]);
+  } else {
+    if (KIND == KIND_PHASE && nonzero2(a0))
+      n0 = a0;
+    else
+      n0 = diag_out(q[0], q[1], a0, q[2], q[3], a1);
+    n1 = diag_out(q[6], q[7], a1, q[4], q[5], a0);
+  }
+  a0 = n0;
+  a1 = n1;
+}
+
+__device__ __forceinline__ void pair_update_kind(int kind, double2 &a0, double2 &a1, const double *q) {
+  if (kind == KIND_GENERAL)
+    pair_update<KIND_GENERAL>(a0, a1, q);
+  else if (kind == KIND_PHASE)
+    pair_update<KIND_PHASE>(a0, a1, q);
+  else
+    pair_update<KIND_DIAG>(a0, a1, q);
+}
+
+// ------------------------------------------------------- register-tiled fused runs
+//
+// One CTA per 2^T tile (T = 9..13), TR = 4 "register qubits": each of the
+// 2^(T-4) threads holds 16 amplitudes in registers, the amplitudes whose tile
+// index has a fixed thread part and all 16 values of the 4 register bits S.
+// A gate whose target is in S is applied entirely in registers; its control
+// may be anywhere: a register bit (per-pair mask), a thread bit (per-thread
+// predicate) or a bit above the tile (per-CTA predicate).  The host splits the
+// gate list into segments with one register set each (greedy look-ahead over
+// upcoming targets); between segments the tile is transposed through shared
+// memory (XOR-swizzled so the 16-B accesses of each quarter warp hit distinct
+// bank groups).  The first segment reuses the natural layout of the coalesced
+// global load when its register set is the top four tile bits, and the last
+// one stores straight to global when it ends in that layout.
+
+constexpr int TR = 4;
+constexpr int TRN = 1 << TR;
+constexpr int TILE_MAX_GATES = 256;
+constexpr int TILE_MAX_SEGS = 64;
+
+struct TileGate {
+  int8_t tb;     // register bit of the target
+  int8_t cmode;  // 0: none, 1: register bit cbit, 2: tile bit cbit (thread part), 3: above the tile
+  int8_t cbit;
+  int8_t kind;
+  int32_t cabove;  // cmode 3: global index bit
+  double q[8];
+};
+
+struct TileSeg {
+  uint8_t S[TR];      // tile bits held in register bits 0..3 (ascending)
+  uint8_t tbits[12];  // tile bit of thread-index bit b
+  int16_t first, count;
+  int8_t natural, pad[3];
+};
+
+struct TileParams {
+  int nsegs;
+  int last_natural;
+  TileSeg seg[TILE_MAX_SEGS];
+  TileGate g[TILE_MAX_GATES];
+};
+
+__device__ __forceinline__ int swz(int i) {
+  int h = i >> 3;
+  h ^= h >> 3;
+  h ^= h >> 6;
+  return i ^ (h & 7);
+}
+
+__device__ __forceinline__ int reg_off(int j, const int m0, const int m1, const int m2, const int m3) {
+  return ((j & 1) ? m0 : 0) | ((j & 2) ? m1 : 0) | ((j & 4) ? m2 : 0) | ((j & 8) ? m3 : 0);
+}
+
+template <int TB>
+__device__ __forceinline__ void tile_gate(double2 (&r)[TRN], uint32_t pm, int kind, const double *q) {
+#pragma unroll
+  for (int j = 0; j < TRN; ++j) {
+    if (j & (1 << TB)) continue;
+    if (!((pm >> j) & 1u)) continue;
+    pair_update_kind(kind, r[j], r[j | (1 << TB)], q);
+  }
+}
+
+template <int T>
+__global__ void __launch_bounds__(1 << (T - TR), (T <= 12) ? 2 : 1)
+    k_tile(double2 *__restrict__ a, const TileParams P) {
+  constexpr int NT = 1 << (T - TR);
+  extern __shared__ double2 s[];
+  const uint64_t tile0 = (uint64_t)blockIdx.x << T;
+  double2 *__restrict__ g = a + tile0;
+  const int tid = threadIdx.x;
+  double2 r[TRN];
+#pragma unroll
+  for (int j = 0; j < TRN; ++j) r[j] = g[tid + j * NT];
+  // current layout: natural (register bits = top four tile bits, thread bits ascending)
+  int cbase = tid, c0 = NT, c1 = NT << 1, c2 = NT << 2, c3 = NT << 3;
+  bool touched = false;
+  for (int sg = 0; sg < P.nsegs; ++sg) {
+    const TileSeg &S = P.seg[sg];
+    const int m0 = 1 << S.S[0], m1 = 1 << S.S[1], m2 = 1 << S.S[2], m3 = 1 << S.S[3];
+    int base = 0;
+#pragma unroll
+    for (int b = 0; b < T - TR; ++b) base |= ((tid >> b) & 1) << S.tbits[b];
+    if (!(sg == 0 && S.natural)) {
+      if (touched) __syncthreads();
+#pragma unroll
+      for (int j = 0; j < TRN; ++j) s[swz(cbase | reg_off(j, c0, c1, c2, c3))] = r[j];
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < TRN; ++j) r[j] = s[swz(base | reg_off(j, m0, m1, m2, m3))];
+      touched = true;
+    }
+    cbase = base;
+    c0 = m0, c1 = m1, c2 = m2, c3 = m3;
+    for (int gi = S.first; gi < S.first + S.count; ++gi) {
+      const TileGate &G = P.g[gi];
+      uint32_t pm = 0xFFFFu;
+      if (G.cmode == 1)
+        pm = G.cbit == 0 ? 0xAAAAu : G.cbit == 1 ? 0xCCCCu : G.cbit == 2 ? 0xF0F0u : 0xFF00u;
+      else if (G.cmode == 2)
+        pm = ((base >> G.cbit) & 1) ? 0xFFFFu : 0u;
+      else if (G.cmode == 3)
+        pm = ((tile0 >> G.cabove) & 1ull) ? 0xFFFFu : 0u;
+      switch (G.tb) {
+        case 0: tile_gate<0>(r, pm, G.kind, G.q); break;
+        case 1: tile_gate<1>(r, pm, G.kind, G.q); break;
+        case 2: tile_gate<2>(r, pm, G.kind, G.q); break;
+        default: tile_gate<3>(r, pm, G.kind, G.q); break;
+      }
+    }
+  }
+  if (!P.last_natural) {
+    if (touched) __syncthreads();
+#pragma unroll
+    for (int j = 0; j < TRN; ++j) s[swz(cbase | reg_off(j, c0, c1, c2, c3))] = r[j];
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < TRN; ++j) r[j] = s[swz(tid + j * NT)];
+  }
+#pragma unroll
+  for (int j = 0; j < TRN; ++j) g[tid + j * NT] = r[j];
+}
+
+// ------------------------------------------------------------ same-target stages
+//
+// A run of gates sharing one target k (any controls, any structure) in one HBM
+// pass: each thread keeps its pairs (i, i + 2^k) in registers and applies the
+// whole list in order -- e.g. a transform stage H(k), R(k, c) for every c < k.
+
+constexpr int STAGE_MAX_GATES = 64;
+
+struct StageGate {
+  int32_t control;  // -1: none
+  int32_t kind;
+  double q[8];
+};
+
+struct StageParams {
+  int ngates;
+  int pad;
+  StageGate g[STAGE_MAX_GATES];
+};
+
+__global__ void __launch_bounds__(BLK) k_stage_pairs(double2 *__restrict__ a, uint64_t npairs, int t,
+                                                     const StageParams P) {
+  const uint64_t tb = 1ull << t;
+  const uint64_t p0 = (uint64_t)blockIdx.x * (BLK * UNROLL) + threadIdx.x;
+  double2 x0[UNROLL], x1[UNROLL];
+  uint64_t i0[UNROLL];
+#pragma unroll
+  for (int u = 0; u < UNROLL; ++u) {
+    const uint64_t p = p0 + (uint64_t)u * BLK;
+    i0[u] = insert_zero(p, t);
+    if (p < npairs) {
+      x0[u] = a[i0[u]];
+      x1[u] = a[i0[u] | tb];
+    }
+  }
+  for (int gi = 0; gi < P.ngates; ++gi) {
+    const StageGate &G = P.g[gi];
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      if (G.control >= 0 && !((i0[u] >> G.control) & 1ull)) continue;
+      pair_update_kind(G.kind, x0[u], x1[u], G.q);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < UNROLL; ++u) {
+    const uint64_t p = p0 + (uint64_t)u * BLK;
+    if (p >= npairs) continue;
+    a[i0[u]] = x0[u];
+    a[i0[u] | tb] = x1[u];
+  }
+}
+
 // ---------------------------------------------------------------- half exchange
 //
 // One rank's side of the pairwise exchange, transfer fused with the update:
@@ -264,6 +495,44 @@ __global__ void __launch_bounds__(BLK) k_exchange(double2 *__restrict__ mine, do
   }
   // Make the remote stores globally performed before the grid retires, so the
   // stream-ordered fence that follows publishes them to the partner.
+  __threadfence_system();
+}
+
+// A whole stage of gates sharing one global target in ONE exchange: every
+// pair crosses NVLink once each way however many gates the stage holds
+// (controls: local bits -> per-element predicate; rank bits were resolved on
+// the host, both partners see the same list).
+__global__ void __launch_bounds__(BLK) k_exchange_stage(double2 *__restrict__ mine, double2 *__restrict__ theirs,
+                                                        uint64_t count, uint64_t base, int own_is_zero,
+                                                        const StageParams P) {
+  const uint64_t p0 = (uint64_t)blockIdx.x * (BLK * UNROLL) + threadIdx.x;
+  double2 x0[UNROLL], x1[UNROLL];
+  uint64_t jj[UNROLL];
+#pragma unroll
+  for (int u = 0; u < UNROLL; ++u) {
+    const uint64_t p = p0 + (uint64_t)u * BLK;
+    jj[u] = base + p;
+    if (p < count) {
+      const double2 am = mine[jj[u]], at = theirs[jj[u]];
+      x0[u] = own_is_zero ? am : at;
+      x1[u] = own_is_zero ? at : am;
+    }
+  }
+  for (int gi = 0; gi < P.ngates; ++gi) {
+    const StageGate &G = P.g[gi];
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      if (G.control >= 0 && !((jj[u] >> G.control) & 1ull)) continue;
+      pair_update_kind(G.kind, x0[u], x1[u], G.q);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < UNROLL; ++u) {
+    const uint64_t p = p0 + (uint64_t)u * BLK;
+    if (p >= count) continue;
+    mine[jj[u]] = own_is_zero ? x0[u] : x1[u];
+    theirs[jj[u]] = own_is_zero ? x1[u] : x0[u];
+  }
   __threadfence_system();
 }
 
@@ -405,6 +674,154 @@ int launch_fused(double2 *a, int m, int T, const FusedParams &P, cudaStream_t st
   }
 }
 
+int classify_kind(const double *q) {
+  const bool z12 = q[2] == 0.0 && q[3] == 0.0, z21 = q[4] == 0.0 && q[5] == 0.0;
+  if (!(z12 && z21)) return KIND_GENERAL;
+  return (q[0] == 1.0 && q[1] == 0.0) ? KIND_PHASE : KIND_DIAG;
+}
+
+// Segment a run of gates (all targets < T, controls anywhere) for k_tile.
+// Greedy: the register set is the next four distinct targets (padded with the
+// natural bits T-1, T-2, ...); a segment extends while targets stay in it.
+// Returns the number of gates planned (limited by the parameter arrays).
+int plan_tile(const sv_gate *gates, int n, int T, TileParams &P) {
+  P.nsegs = 0;
+  int gi = 0;
+  while (gi < n && gi < TILE_MAX_GATES && P.nsegs < TILE_MAX_SEGS) {
+    int S[TR], ns = 0;
+    auto in_s = [&](int b) {
+      for (int i = 0; i < ns; ++i)
+        if (S[i] == b) return true;
+      return false;
+    };
+    for (int j = gi; j < n && ns < TR; ++j)
+      if (!in_s(gates[j].target)) S[ns++] = gates[j].target;
+    for (int b = T - 1; b >= 0 && ns < TR; --b)
+      if (!in_s(b)) S[ns++] = b;
+    std::sort(S, S + TR);
+    TileSeg &seg = P.seg[P.nsegs];
+    memset(&seg, 0, sizeof(seg));
+    int L[16], nl = 0;
+    for (int b = 0; b < T; ++b)
+      if (!in_s(b)) L[nl++] = b;
+    // thread bits 0..2 (one quarter warp) on tile bits of distinct residue mod 3:
+    // with the swizzle, the quarter warp's 16-B accesses then hit 8 bank groups.
+    bool used[16] = {};
+    int nt = 0;
+    for (int res = 0; res < 3; ++res)
+      for (int i = 0; i < nl; ++i)
+        if (!used[i] && L[i] % 3 == res) {
+          used[i] = true;
+          seg.tbits[nt++] = (uint8_t)L[i];
+          break;
+        }
+    for (int i = 0; i < nl; ++i)
+      if (!used[i]) seg.tbits[nt++] = (uint8_t)L[i];
+    bool natural = true;
+    for (int b = 0; b < TR; ++b) natural &= S[b] == T - TR + b;
+    for (int b = 0; b < T - TR; ++b) natural &= seg.tbits[b] == b;
+    for (int b = 0; b < TR; ++b) seg.S[b] = (uint8_t)S[b];
+    seg.natural = natural ? 1 : 0;
+    seg.first = (int16_t)gi;
+    while (gi < n && gi < TILE_MAX_GATES && in_s(gates[gi].target)) {
+      const sv_gate &src = gates[gi];
+      TileGate &G = P.g[gi];
+      memset(&G, 0, sizeof(G));
+      for (int b = 0; b < TR; ++b)
+        if (S[b] == src.target) G.tb = (int8_t)b;
+      const int c = src.control;
+      if (c < 0) {
+        G.cmode = 0;
+      } else if (in_s(c)) {
+        G.cmode = 1;
+        for (int b = 0; b < TR; ++b)
+          if (S[b] == c) G.cbit = (int8_t)b;
+      } else if (c < T) {
+        G.cmode = 2;
+        G.cbit = (int8_t)c;
+      } else {
+        G.cmode = 3;
+        G.cabove = c;
+      }
+      G.kind = (int8_t)classify_kind(src.q);
+      memcpy(G.q, src.q, sizeof(G.q));
+      ++gi;
+    }
+    seg.count = (int16_t)(gi - seg.first);
+    ++P.nsegs;
+  }
+  P.last_natural = P.seg[P.nsegs - 1].natural;
+  return gi;
+}
+
+template <int T>
+int launch_tile_t(double2 *a, int m, const TileParams &P, cudaStream_t st) {
+  const size_t smem = sizeof(double2) << T;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_tile<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return fail(SV_ECUDA, "tile: smem attribute: %s", cudaGetErrorString(e));
+  }
+  k_tile<T><<<(unsigned)(1ull << (m - T)), 1 << (T - TR), smem, st>>>(a, P);
+  return after_launch("k_tile");
+}
+
+int launch_tile(double2 *a, int m, int T, const TileParams &P, cudaStream_t st) {
+  switch (T) {
+    case 9: return launch_tile_t<9>(a, m, P, st);
+    case 10: return launch_tile_t<10>(a, m, P, st);
+    case 11: return launch_tile_t<11>(a, m, P, st);
+    case 12: return launch_tile_t<12>(a, m, P, st);
+    case 13: return launch_tile_t<13>(a, m, P, st);
+    default: return fail(SV_EINVAL, "tile exponent %d unsupported", T);
+  }
+}
+
+// Run gates (targets < T, controls anywhere) through k_tile, as many launches as
+// the parameter arrays need.
+int run_tile(double2 *a, int m, int T, const sv_gate *gates, int n, cudaStream_t st) {
+  static thread_local TileParams P;  // ~20 KB: keep it off the stack
+  int off = 0;
+  while (off < n) {
+    const int used = plan_tile(gates + off, n - off, T, P);
+    const int rc = launch_tile(a, m, T, P, st);
+    if (rc != SV_OK) return rc;
+    off += used;
+  }
+  return SV_OK;
+}
+
+int launch_gate(double2 *a, int m, const sv_gate &g, cudaStream_t st) {
+  const GateQ q = load_q(g.q);
+  if (g.control < 0) return launch_local<MODE_SINGLE>(a, m, g.target, 0, q, st, "single");
+  if (g.control == 0) return launch_local<MODE_PRED>(a, m, g.target, 0, q, st, "controlled");
+  const int tv = g.target < g.control ? g.target : g.target - 1;
+  return launch_local<MODE_CTL>(a, m - 1, tv, g.control, q, st, "controlled");
+}
+
+int run_stage(double2 *a, int m, const sv_gate *gates, int n, cudaStream_t st) {
+  static thread_local StageParams P;
+  const int t = gates[0].target;
+  P.ngates = n;
+  for (int i = 0; i < n; ++i) {
+    P.g[i].control = gates[i].control;
+    P.g[i].kind = classify_kind(gates[i].q);
+    memcpy(P.g[i].q, gates[i].q, sizeof(P.g[i].q));
+  }
+  const uint64_t np = 1ull << (m - 1);
+  k_stage_pairs<<<grid_for(np, BLK * UNROLL), BLK, 0, st>>>(a, np, t, P);
+  return after_launch("k_stage_pairs");
+}
+
+int check_gates(const char *who, int m, const sv_gate *gates, int n, int tmax) {
+  for (int i = 0; i < n; ++i) {
+    const sv_gate &g = gates[i];
+    if (g.target < 0 || g.target >= tmax || g.control < -1 || g.control >= m || g.control == g.target)
+      return fail(SV_EINVAL, "%s: gate %d (t=%d, c=%d) invalid for m=%d (targets < %d)", who, i, g.target,
+                  g.control, m, tmax);
+  }
+  return SV_OK;
+}
+
 typedef CUresult (*PFN_getAddressRange)(CUdeviceptr *, size_t *, CUdeviceptr);
 
 int alloc_base(const void *ptr, uintptr_t *base) {
@@ -465,20 +882,75 @@ int sv_apply_fused(void *amps, int m, int l, const sv_gate *gates, int ngates, v
   if (l < 1 || l > lmax) return fail(SV_EINVAL, "sv_apply_fused: block exponent %d not in [1, %d]", l, lmax);
   if (ngates < 1 || ngates > SV_FUSED_MAX_GATES)
     return fail(SV_EINVAL, "sv_apply_fused: %d gates not in [1, %d]", ngates, SV_FUSED_MAX_GATES);
-  static thread_local FusedParams P;  // 18 KB: keep it off the stack
-  P.ngates = ngates;
-  P.pad = 0;
   for (int i = 0; i < ngates; ++i) {
     const sv_gate &g = gates[i];
     if (g.target < 0 || g.target >= l || g.control >= l || g.control < -1 || g.control == g.target)
       return fail(SV_EINVAL, "sv_apply_fused: gate %d (t=%d, c=%d) outside block exponent %d", i, g.target,
                   g.control, l);
-    P.g[i] = g;
   }
-  // Tile: at least 2^12 amplitudes per CTA where the slice allows (occupancy:
-  // 64 KiB tiles give 3 CTAs/SM), never below the block exponent.
-  int T = l > 12 ? l : (m < 12 ? m : 12);
+  // Tile: 2^12 amplitudes per CTA where the slice allows (64 KiB: two CTAs per
+  // SM overlap one tile's HBM traffic with the other's gates), never below l.
+  const int T = l > 12 ? l : (m < 12 ? m : 12);
+  if (T >= 9) return run_tile((double2 *)amps, m, T, gates, ngates, (cudaStream_t)stream);
+  static thread_local FusedParams P;  // 18 KB: keep it off the stack
+  P.ngates = ngates;
+  P.pad = 0;
+  for (int i = 0; i < ngates; ++i) P.g[i] = gates[i];
   return launch_fused((double2 *)amps, m, T, P, (cudaStream_t)stream);
+}
+
+int sv_apply_gates(void *amps, int m, const sv_gate *gates, int ngates, int tile, void *stream) {
+  if (bad_ptr(amps) || (!gates && ngates)) return fail(SV_EINVAL, "sv_apply_gates: null or misaligned pointer");
+  if (m < 1 || m > 62) return fail(SV_EINVAL, "sv_apply_gates: m=%d out of range", m);
+  if (ngates < 0) return fail(SV_EINVAL, "sv_apply_gates: negative gate count");
+  int rc = check_gates("sv_apply_gates", m, gates, ngates, m);
+  if (rc != SV_OK) return rc;
+  const int tmax = m < SV_FUSED_MAX_TILE ? m : SV_FUSED_MAX_TILE;
+  const int T = tile > 0 ? tile : tmax;
+  if (tile != 0 && (tile < 9 || tile > tmax)) return fail(SV_EINVAL, "sv_apply_gates: tile %d not in [9, %d]", tile, tmax);
+  double2 *a = (double2 *)amps;
+  cudaStream_t st = (cudaStream_t)stream;
+  int i = 0;
+  while (i < ngates && rc == SV_OK) {
+    const int t = gates[i].target;
+    int j = i + 1;
+    if (T >= 9 && t < T) {
+      while (j < ngates && gates[j].target < T) ++j;
+      rc = (j - i == 1) ? launch_gate(a, m, gates[i], st) : run_tile(a, m, T, gates + i, j - i, st);
+    } else {
+      while (j < ngates && gates[j].target == t && j - i < STAGE_MAX_GATES) ++j;
+      if (j - i == 1 || t < 5) {
+        for (int k = i; k < j && rc == SV_OK; ++k) rc = launch_gate(a, m, gates[k], st);
+      } else {
+        rc = run_stage(a, m, gates + i, j - i, st);
+      }
+    }
+    i = j;
+  }
+  return rc;
+}
+
+int sv_exchange_stage(void *mine, void *theirs, int m, int own_is_zero, const sv_gate *gates, int ngates,
+                      void *stream) {
+  if (bad_ptr(mine) || bad_ptr(theirs) || !gates)
+    return fail(SV_EINVAL, "sv_exchange_stage: null or misaligned pointer");
+  if (mine == theirs) return fail(SV_EINVAL, "sv_exchange_stage: partner slice aliases the local slice");
+  if (m < 1 || m > 62) return fail(SV_EINVAL, "sv_exchange_stage: m=%d out of range", m);
+  if (ngates < 1 || ngates > STAGE_MAX_GATES)
+    return fail(SV_EINVAL, "sv_exchange_stage: %d gates not in [1, %d]", ngates, STAGE_MAX_GATES);
+  static thread_local StageParams P;
+  P.ngates = ngates;
+  for (int i = 0; i < ngates; ++i) {
+    if (gates[i].control < -1 || gates[i].control >= m)
+      return fail(SV_EINVAL, "sv_exchange_stage: gate %d control %d is not a local qubit", i, gates[i].control);
+    P.g[i].control = gates[i].control;
+    P.g[i].kind = classify_kind(gates[i].q);
+    memcpy(P.g[i].q, gates[i].q, sizeof(P.g[i].q));
+  }
+  const uint64_t half = 1ull << (m - 1);
+  k_exchange_stage<<<grid_for(half, BLK * UNROLL), BLK, 0, (cudaStream_t)stream>>>(
+      (double2 *)mine, (double2 *)theirs, half, own_is_zero ? 0 : half, own_is_zero ? 1 : 0, P);
+  return after_launch("sv_exchange_stage");
 }
 
 int sv_exchange(void *mine, void *theirs, int m, int own_is_zero, int c_local, const double *q, void *stream) {

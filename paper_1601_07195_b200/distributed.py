@@ -207,6 +207,19 @@ class CudaExecutor:
             _lib.check(_lib.load().sv_exchange(ptr, theirs, m, int(own_is_zero), int(c_local),
                                                _as_gate(q).qbuf(), stream_handle()))
 
+    def exchange_stage(self, state: LocalState, theirs: int, own_is_zero: bool, ops) -> None:
+        from .kernels import gate_array
+
+        ptr, m = device_view(state.amps)
+        with torch.cuda.device(state.amps.device):
+            _lib.check(_lib.load().sv_exchange_stage(ptr, theirs, m, int(own_is_zero), gate_array(ops), len(ops),
+                                                     stream_handle()))
+
+    def local_gates(self, state: LocalState, ops, tile: int = 0) -> None:
+        from .kernels import apply_gates
+
+        apply_gates(state.amps, ops, tile)
+
     def synchronize(self, state: LocalState) -> None:
         torch.cuda.current_stream(state.amps.device).synchronize()
 

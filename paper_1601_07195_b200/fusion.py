@@ -27,10 +27,15 @@ GPU_MAX_BLOCK_EXPONENT = _lib.SV_FUSED_MAX_TILE
 
 @dataclass(frozen=True)
 class FusionConfig:
-    """l_c: block exponent (blocks of 2^l_c amplitudes)."""
+    """l_c: block exponent (blocks of 2^l_c amplitudes).
+
+    ``passes=True`` (an extension, off by default so plans match the
+    reference) replaces block runs by the native pass planner of passes.py:
+    l_c then sets the register tile (clamped to [9, 13])."""
 
     l_c: int
     enabled: bool = True
+    passes: bool = False
 
     def __post_init__(self):
         if self.l_c < 1:
@@ -63,6 +68,7 @@ class PassThrough:
 class FusionPlan:
     l_c: int
     segments: list = field(default_factory=list)
+    passes: bool = False
 
     def flatten(self) -> list[GateOp]:
         out: list[GateOp] = []
@@ -76,7 +82,10 @@ class FusionPlan:
 
 def plan_fusion(circuit: Circuit, config: FusionConfig) -> FusionPlan:
     """Greedy maximal runs in circuit order, no reordering (fusion.py:71-94)."""
-    plan = FusionPlan(config.l_c)
+    plan = FusionPlan(config.l_c, passes=config.enabled and config.passes)
+    if plan.passes:  # the pass planner needs m; execute_plan cuts the passes
+        plan.segments = [PassThrough(op) for op in circuit]
+        return plan
     run: list[GateOp] = []
     for op in circuit:
         if config.enabled and op.max_qubit() < config.l_c:
@@ -130,6 +139,13 @@ def run_fused(state: LocalState, gates, l_c: int) -> int:
 def execute_plan(state: LocalState, plan: FusionPlan, policy: ThreadPolicy = SERIAL, transport=None, *,
                  chunk_amps: int | None = None, scratch: ScratchPool | None = None) -> None:
     """Fused runs as tile passes, pass-throughs through apply_op (fusion.py:97-135)."""
+    if plan.passes:
+        from .passes import execute_pass, plan_passes, tile_for
+
+        tile = tile_for(plan.l_c, state.layout.m)
+        for p in plan_passes(plan.flatten(), state.layout.m):
+            execute_pass(state, p, transport, tile=tile)
+        return
     if plan.l_c > state.layout.m:
         raise FusionContractError(f"block exponent {plan.l_c} exceeds local qubit count m={state.layout.m}")
     for seg in plan.segments:

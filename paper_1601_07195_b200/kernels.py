@@ -203,6 +203,21 @@ def launch_fused(amps, ops: list, l: int) -> None:
             _lib.check(lib.sv_apply_fused(ptr, m, int(l), gate_array(part), len(part), stream_handle()))
 
 
+def apply_gates(amps, ops, tile: int = 0) -> None:
+    """Native pass planner (sv_apply_gates): local gates applied in order, grouped into
+    register-tiled runs (targets < tile, controls anywhere) and same-target stage passes.
+    Bit-identical to applying them one by one."""
+    ptr, m = device_view(amps)
+    ops = list(ops)
+    if not ops:
+        return
+    for op in ops:
+        if op.max_qubit() >= m:
+            raise LayoutError(f"gate on qubits {op.qubits()} is not local (m={m})")
+    with torch.cuda.device(amps.device):
+        _lib.check(_lib.load().sv_apply_gates(ptr, m, gate_array(ops), len(ops), int(tile), stream_handle()))
+
+
 def apply_block(block_amps, gates: Iterable["GateOp"], policy: ThreadPolicy = SERIAL) -> None:
     """Apply gates in order to one contiguous 2^b slice as a b-qubit state (kernels.py:225-240).
 

@@ -1,0 +1,111 @@
+"""Pass fusion: the native planner behind ``FusionConfig(passes=True)``.
+
+The reference fuses only runs of gates whose qubits all sit below l_c
+(fusion.py:71-94); every other gate is its own sweep over memory.  With
+``passes=True`` the circuit is cut into as few HBM passes as the kernels
+allow, without reordering any gate:
+
+* ``local`` pass -- a maximal run of gates with a local target (controls
+  anywhere; a control in the rank bits turns into "uncontrolled" or "skip" on
+  this rank).  Executed by ``sv_apply_gates``: register-tiled runs for
+  targets below the tile (2^13), one same-target stage pass for each run of
+  gates sharing a higher target (a transform stage H(k), R(k, c) for all c
+  is ONE pass), single-gate kernels otherwise.
+* ``global_stage`` -- a run of gates sharing one global target: ONE fused
+  NVLink exchange applies them all (``sv_exchange_stage``).
+* ``global_gate`` -- a lone global-target gate: the reference-equivalent
+  exchange (``apply_global``, per-gate traffic contract preserved).
+
+Results are bit-identical to the reference's unfused execution: every pair
+sees the same updates in the same order, and the structure-specialised
+updates (diagonal / phase gates) are exact (svb200.cu "pair update").
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+from . import _lib
+from .circuits import GateOp
+from .distributed import _CUDA, _check_transport, apply_global
+from .errors import LayoutError
+from .kernels import _as_gate
+
+
+@dataclass(frozen=True)
+class Pass:
+    kind: str                # "local" | "global_stage" | "global_gate"
+    gates: tuple[GateOp, ...]
+    target: int | None = None
+
+
+def plan_passes(gates, m: int) -> list[Pass]:
+    """Cut a gate sequence into passes (pure function of the gates and m: identical on every rank)."""
+    gates = list(gates)
+    out: list[Pass] = []
+    i, n = 0, len(gates)
+    while i < n:
+        t = gates[i].target
+        j = i + 1
+        if t < m:
+            while j < n and gates[j].target < m:
+                j += 1
+            out.append(Pass("local", tuple(gates[i:j])))
+        else:
+            while j < n and gates[j].target == t and j - i < _lib.SV_STAGE_MAX_GATES:
+                j += 1
+            out.append(Pass("global_stage" if j - i > 1 else "global_gate", tuple(gates[i:j]), t))
+        i = j
+    return out
+
+
+def _resolve_rank_controls(ops, layout) -> list[GateOp]:
+    """Gates whose control is a rank bit become uncontrolled (bit set) or vanish (bit clear)."""
+    out = []
+    for op in ops:
+        c = op.control
+        if c is not None and c >= layout.m:
+            if (layout.rank >> (c - layout.m)) & 1:
+                out.append(GateOp(op.gate, op.target, None, op.name))
+        else:
+            out.append(op)
+    return out
+
+
+def execute_pass(state, p: Pass, transport=None, *, tile: int = 0, executor=None) -> None:
+    lay = state.layout
+    ex = executor or (transport.executor if transport is not None else _CUDA)
+    if p.kind == "local":
+        ops = _resolve_rank_controls(p.gates, lay)
+        if ops:
+            ex.local_gates(state, ops, tile)
+        return
+    if transport is None:
+        raise LayoutError(f"gate on qubit {p.target} >= m={lay.m} requires a transport")
+    if p.kind == "global_gate":
+        op = p.gates[0]
+        apply_global(state, op.target, op.control, op.gate, transport, executor=executor)
+        return
+    _check_transport(transport, lay)
+    transport.fresh_tag()
+    transport.ensure_registered(state)
+    bit = p.target - lay.m
+    partner = lay.rank ^ (1 << bit)
+    zero = ((lay.rank >> bit) & 1) == 0
+    ops = [GateOp(_as_gate(op.gate), op.target, op.control, op.name)
+           for op in _resolve_rank_controls(p.gates, lay)]
+    try:
+        transport.barrier(state)
+        if ops:
+            ex.exchange_stage(state, transport.peer_pointer(state, partner), zero, ops)
+            transport.count(1 << (lay.m + 4), 1 << (lay.m + 4))
+        transport.barrier(state)
+    except BaseException:
+        state.corrupt = True
+        raise
+
+
+def tile_for(l_c: int, m: int) -> int:
+    """Tile exponent of the register-tiled kernel for a FusionConfig block exponent."""
+    t = min(l_c, m, _lib.SV_FUSED_MAX_TILE)
+    return t if t >= 9 else 0

@@ -1,0 +1,158 @@
+"""GPU: register-tiled runs, same-target stages, structure-specialised updates and pass fusion.
+
+Strictest bar: the raw bit patterns (sign of zero included) equal the oracle's
+unfused, unspecialised evaluation of the reference arithmetic.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import random_state
+from test_gpu_exchange import run_loopback
+
+pytestmark = pytest.mark.gpu
+
+sv = pytest.importorskip("paper_1601_07195_b200")
+from oracle import oracle  # noqa: E402
+
+DEV = "cuda:0"
+
+
+def bits_equal(a, b):
+    return np.array_equal(np.ascontiguousarray(a).view(np.uint64), np.ascontiguousarray(b).view(np.uint64))
+
+
+def with_zeros(rng, n, frac=0.15):
+    """Random state with some exact +-0 components (exercises the exact-zero branches)."""
+    v = random_state(rng, n)
+    f = v.view(np.float64).copy()
+    hit = rng.random(f.shape) < frac
+    f[hit] = np.where(rng.random(hit.sum()) < 0.5, 0.0, -0.0)
+    return f.view(np.complex128)
+
+
+def gate_zoo(rng):
+    """General, diagonal, phase (incl. -0 imaginary parts), real and anti-diagonal matrices."""
+    th = rng.uniform(0, 2 * np.pi)
+    return [
+        sv.random_unitary(rng), sv.hadamard(), sv.phase_r(int(rng.integers(1, 9))),
+        sv.phase_r(int(rng.integers(1, 9))).dagger(), sv.rotation_z(th), sv.pauli_z(), sv.pauli_x(),
+        sv.GateMatrix([[np.exp(1j * th), 0], [0, np.exp(-2j * th)]]), sv.pauli_y(), sv.rotation_y(th),
+    ]
+
+
+def random_ops(rng, n, count, tmax, cfrac=0.5, zoo=True):
+    ops = []
+    for _ in range(count):
+        g = gate_zoo(rng)[int(rng.integers(10))] if zoo and rng.random() < 0.6 else sv.random_unitary(rng)
+        t = int(rng.integers(tmax))
+        c = None
+        if rng.random() < cfrac:
+            c = int(rng.integers(n - 1))
+            c = c + 1 if c >= t else c
+        ops.append(sv.GateOp(g, t, c))
+    return ops
+
+
+def run_oracle(v, ops):
+    w = v.copy()
+    oracle.run_circuit(w, ops, threads=8)
+    return w
+
+
+@pytest.mark.parametrize("n,T", [(9, 9), (12, 12), (13, 13), (16, 12), (16, 13), (18, 10)])
+def test_tile_runs_bitwise(n, T):
+    rng = np.random.default_rng(1000 + 17 * n + T)
+    for trial in range(3):
+        v = with_zeros(rng, n) if trial else random_state(rng, n)
+        ops = random_ops(rng, n, 120, T)
+        a = torch.from_numpy(v.copy()).to(DEV)
+        sv.kernels.apply_gates(a, ops, tile=T)
+        torch.cuda.synchronize()
+        assert bits_equal(a.cpu().numpy(), run_oracle(v, ops)), (n, T, trial)
+
+
+def test_tile_register_set_transitions_and_natural_layout():
+    """Target sequences that hit the natural layout, force many transposes, or repeat one target."""
+    n = 14
+    rng = np.random.default_rng(5)
+    v = with_zeros(rng, n)
+    for targets in ([12, 11, 10, 9] * 5, list(range(13)) * 3, [0] * 40, [3, 12, 0, 7, 12, 1, 9, 4, 11, 2, 5],
+                    [12, 11, 10, 9, 0, 12]):
+        ops = [sv.GateOp(sv.random_unitary(rng), t, None if i % 3 else (t + 5) % n) for i, t in enumerate(targets)]
+        a = torch.from_numpy(v.copy()).to(DEV)
+        sv.kernels.apply_gates(a, ops, tile=13)
+        torch.cuda.synchronize()
+        assert bits_equal(a.cpu().numpy(), run_oracle(v, ops)), targets
+
+
+@pytest.mark.parametrize("n", [14, 20])
+def test_stage_passes_and_mixed_lists_bitwise(n):
+    rng = np.random.default_rng(n)
+    v = with_zeros(rng, n)
+    ops = []
+    for k in (n - 1, 15, 13, 9, 4):  # stages on high and low targets, any controls
+        k = min(k, n - 1)
+        ops.append(sv.GateOp(sv.hadamard(), k))
+        ops += [sv.GateOp(g, k, c) for c, g in zip(rng.permutation([c for c in range(n) if c != k])[:7],
+                                                     gate_zoo(rng))]
+    ops += random_ops(rng, n, 60, n)
+    a = torch.from_numpy(v.copy()).to(DEV)
+    sv.kernels.apply_gates(a, ops)
+    torch.cuda.synchronize()
+    assert bits_equal(a.cpu().numpy(), run_oracle(v, ops))
+
+
+@pytest.mark.parametrize("n", [12, 16, 21])
+def test_qft_iqft_pass_fusion_bitwise(n):
+    rng = np.random.default_rng(70 + n)
+    for build in (sv.build_qft, sv.build_iqft):
+        circ = build(n)
+        for v in (random_state(rng, n), np.eye(1, 1 << n, int(rng.integers(1 << n)), dtype=np.complex128)[0]):
+            want = run_oracle(v, circ.gates)
+            for l_c in (9, 12, 13):
+                st = sv.state_from_global(sv.Layout(n), v, device=DEV)
+                sv.run_circuit(st, circ, fusion=sv.FusionConfig(l_c=l_c, passes=True))
+                assert bits_equal(st.to_numpy(), want), (build.__name__, l_c)
+
+
+def test_passes_records_and_golden(golden):
+    d = golden("circuits_small")
+    from conftest import golden_circuit
+
+    for name, n in (("mix10", 10), ("ctl12", 12)):
+        circ = golden_circuit(d, name, n)
+        st = sv.state_from_global(sv.Layout(n), d[f"{name}_in"], device=DEV)
+        recs = sv.run_circuit(st, circ, fusion=sv.FusionConfig(l_c=13, passes=True), record=True)
+        assert np.array_equal(st.to_numpy(), d[f"{name}_out"])
+        assert sum(r.gate_count for r in recs) == len(circ)
+        assert all(r.seconds > 0 for r in recs)
+
+
+@pytest.mark.parametrize("p", [1, 2, 3])
+def test_loopback_global_stages_bitwise(p):
+    """Transform stages on global targets: one exchange per stage, bits equal to the oracle."""
+    n = 14
+    rng = np.random.default_rng(300 + p)
+    v = with_zeros(rng, n)
+    circ = sv.build_qft(n)
+    circ.extend(random_ops(rng, n, 40, n))
+    want = run_oracle(v, circ.gates)
+    got, _ = run_loopback(n, p, circ, v, fusion=sv.FusionConfig(l_c=9, passes=True))
+    assert bits_equal(got, want)
+
+
+def test_exchange_stage_abi_guards():
+    from paper_1601_07195_b200 import _lib
+
+    a = torch.zeros(64, dtype=torch.complex128, device=DEV)
+    b = torch.zeros(64, dtype=torch.complex128, device=DEV)
+    g = sv.kernels.gate_array([sv.GateOp(sv.hadamard(), 6, 7)])
+    st = torch.cuda.current_stream().cuda_stream
+    L = _lib.load()
+    assert L.sv_exchange_stage(a.data_ptr(), b.data_ptr(), 6, 1, g, 1, st) == _lib.SV_EINVAL  # control 7 not local
+    assert L.sv_exchange_stage(a.data_ptr(), b.data_ptr(), 6, 1, g, 0, st) == _lib.SV_EINVAL
+    assert L.sv_apply_gates(a.data_ptr(), 6, g, 1, 0, st) == _lib.SV_EINVAL  # target 6 not local

@@ -1,0 +1,90 @@
+"""Per-placement throughput sweep on one GPU (diagnostics; bench.py is the contract).
+
+    python tools/gate_sweep.py [--n 30] [--reps 5] [--what single,controlled,fused,qft,config1]
+
+Prints one JSON object per measurement: kernel class, placement, median ms, GB/s against the
+reference's algorithmic accounting (32*2^m single, 16*2^m controlled, 32*2^m physical for a
+fused run plus G*32*2^m effective).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import paper_1601_07195_b200 as sv  # noqa: E402
+
+
+def timeit(fn, reps):
+    st = torch.cuda.current_stream()
+    ts = []
+    for _ in range(reps + 1):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        fn()
+        b.record(st)
+        b.synchronize()
+        ts.append(a.elapsed_time(b))
+    return float(np.median(ts[1:]))
+
+
+def emit(**kw):
+    print(json.dumps(kw), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n", type=int, default=30)
+    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--what", default="single,controlled,fused,qft,config1")
+    a = ap.parse_args()
+    what = set(a.what.split(","))
+    n = a.n
+    torch.cuda.set_device(0)
+    st = sv.init_random_state(sv.Layout(n), seed=1)
+    rng = np.random.default_rng(0)
+    q = sv.random_unitary(rng)
+    if "single" in what:
+        for k in range(n):
+            ms = timeit(lambda: sv.apply_single_raw(st.amps, k, q), a.reps)
+            emit(kind="single", k=k, ms=round(ms, 4), gbps=round((32 << n) / ms / 1e6, 1))
+    if "controlled" in what:
+        pairs = [(c, t) for c in (0, 1, 2, 3, 4, 5, 6, 10, 15, 20, n - 2, n - 1)
+                 for t in (0, 1, 2, 4, 5, 8, 15, n - 1) if c != t and c < n and t < n]
+        for c, t in pairs:
+            ms = timeit(lambda: sv.apply_controlled_raw(st.amps, c, t, q), a.reps)
+            emit(kind="controlled", c=c, t=t, ms=round(ms, 4), gbps=round((16 << n) / ms / 1e6, 1))
+    if "fused" in what:
+        for G in (1, 2, 4, 8, 16, 32, 64):
+            for lmax in (5, 12, 13):
+                gates = [sv.GateOp(sv.random_unitary(rng), int(rng.integers(lmax))) for _ in range(G)]
+                ms = timeit(lambda: sv.run_fused(st, gates, lmax), a.reps)
+                emit(kind="fused", gates=G, lmax=lmax, ms=round(ms, 4), phys_gbps=round((32 << n) / ms / 1e6, 1),
+                     eff_gbps=round(G * (32 << n) / ms / 1e6, 1))
+    if "qft" in what:
+        circ = sv.build_qft(n)
+        for l_c in (None, 12, 13):
+            fusion = None if l_c is None else sv.FusionConfig(l_c=l_c)
+            ms = timeit(lambda: sv.run_circuit(st, circ, fusion=fusion), max(1, a.reps // 2))
+            eff = sum((32 if op.control is None else 16) << n for op in circ)
+            emit(kind="qft", n=n, l_c=l_c, gates=len(circ), ms=round(ms, 3), eff_gbps=round(eff / ms / 1e6, 1),
+                 ms_per_gate=round(ms / len(circ), 4))
+    if "config1" in what:
+        m = 20
+        s20 = sv.init_random_state(sv.Layout(m), seed=2)
+        circ = sv.random_circuit(m, 200, np.random.default_rng(1), controlled_fraction=0.0)
+        for l_c in (None, 12, 13):
+            fusion = None if l_c is None else sv.FusionConfig(l_c=l_c)
+            ms = timeit(lambda: sv.run_circuit(s20, circ, fusion=fusion), a.reps)
+            emit(kind="config1", n=m, l_c=l_c, gates=200, ms=round(ms, 3), us_per_gate=round(ms * 1e3 / 200, 2),
+                 eff_gbps=round(200 * (32 << m) / ms / 1e6, 1))
+
+
+if __name__ == "__main__":
+    main()
