@@ -239,7 +239,9 @@ __global__ void __launch_bounds__(FusedShape<T>::NT) k_fused(double2 *__restrict
 enum { KIND_GENERAL = 0, KIND_DIAG = 1, KIND_PHASE = 2 };
 
 __device__ __forceinline__ bool nonzero2(double2 v) {
-  return ((__double_as_longlong(v.x) << 1) != 0) & ((__double_as_longlong(v.y) << 1) != 0);
+  const int mx = (__double2hiint(v.x) & 0x7fffffff) | __double2loint(v.x);
+  const int my = (__double2hiint(v.y) & 0x7fffffff) | __double2loint(v.y);
+  return (mx != 0) & (my != 0);
 }
 
 __device__ __forceinline__ double2 diag_out(double rr, double ri, double2 self, double zr, double zi,
@@ -332,14 +334,79 @@ __device__ __forceinline__ int reg_off(int j, const int m0, const int m1, const 
   return ((j & 1) ? m0 : 0) | ((j & 2) ? m1 : 0) | ((j & 4) ? m2 : 0) | ((j & 8) ? m3 : 0);
 }
 
+// The 8 register pairs of a gate on register bit TB, processed in groups of
+// TG; for diagonal/phase gates the zero tests of a group are merged into one
+// branch (see stage_gate).  FULL: every pair active (pm == 0xFFFF).
+constexpr int TG = 2;
+
+template <int TB, int KIND, bool FULL>
+__device__ __forceinline__ void tile_gate_k(double2 (&r)[TRN], uint32_t pm, const double *qp) {
+  double q[8];  // once per gate in registers, not one constant-bank load per pair
+#pragma unroll
+  for (int i = 0; i < 8; ++i) q[i] = qp[i];
+#define PAIRS(k) ((((k) >> TB) << (TB + 1)) | ((k) & ((1 << TB) - 1)))  // k-th j with bit TB clear
+#pragma unroll
+  for (int grp = 0; grp < 8 / TG; ++grp) {
+    if (KIND == KIND_GENERAL) {
+#pragma unroll
+      for (int k = 0; k < TG; ++k) {
+        const int j = PAIRS(grp * TG + k);
+        if (FULL || ((pm >> j) & 1u)) pair_update<KIND_GENERAL>(r[j], r[j | (1 << TB)], q);
+      }
+    } else {
+      double2 n0[TG], n1[TG];
+      bool bad = false;
+#pragma unroll
+      for (int k = 0; k < TG; ++k) {
+        const int j = PAIRS(grp * TG + k);
+        const bool act = FULL || ((pm >> j) & 1u);
+        n0[k] = KIND == KIND_PHASE ? r[j] : cmul(q[0], q[1], r[j]);
+        n1[k] = cmul(q[6], q[7], r[j | (1 << TB)]);
+        bad |= act & !(nonzero2(n0[k]) & nonzero2(n1[k]));
+      }
+      if (bad) {
+#pragma unroll
+        for (int k = 0; k < TG; ++k) {
+          const int j = PAIRS(grp * TG + k);
+          if (FULL || ((pm >> j) & 1u)) pair_update<KIND_GENERAL>(r[j], r[j | (1 << TB)], q);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < TG; ++k) {
+          const int j = PAIRS(grp * TG + k);
+          if (FULL || ((pm >> j) & 1u)) {
+            r[j] = n0[k];
+            r[j | (1 << TB)] = n1[k];
+          }
+        }
+      }
+    }
+  }
+}
+
+template <int TB, int KIND>
+__device__ __forceinline__ void tile_gate_all(double2 (&r)[TRN], const double *qp) {
+  tile_gate_k<TB, KIND, true>(r, 0xFFFFu, qp);
+}
+
 template <int TB>
 __device__ __forceinline__ void tile_gate(double2 (&r)[TRN], uint32_t pm, int kind, const double *q) {
-#pragma unroll
-  for (int j = 0; j < TRN; ++j) {
-    if (j & (1 << TB)) continue;
-    if (!((pm >> j) & 1u)) continue;
-    pair_update_kind(kind, r[j], r[j | (1 << TB)], q);
+  if (pm == 0u) return;
+  if (pm == 0xFFFFu) {  // uncontrolled, or control decided per thread/CTA: straight-line code
+    if (kind == KIND_GENERAL)
+      tile_gate_all<TB, KIND_GENERAL>(r, q);
+    else if (kind == KIND_PHASE)
+      tile_gate_all<TB, KIND_PHASE>(r, q);
+    else
+      tile_gate_all<TB, KIND_DIAG>(r, q);
+    return;
   }
+  if (kind == KIND_GENERAL)
+    tile_gate_k<TB, KIND_GENERAL, false>(r, pm, q);
+  else if (kind == KIND_PHASE)
+    tile_gate_k<TB, KIND_PHASE, false>(r, pm, q);
+  else
+    tile_gate_k<TB, KIND_DIAG, false>(r, pm, q);
 }
 
 template <int T>
@@ -422,14 +489,77 @@ struct StageParams {
   StageGate g[STAGE_MAX_GATES];
 };
 
+constexpr int SUNROLL = 4;
+
+template <int KIND, int U>
+__device__ __forceinline__ void stage_gate(double2 (&x0)[U], double2 (&x1)[U], const uint64_t (&idx)[U],
+                                           uint64_t cm, const double *qp) {
+  double q[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) q[i] = qp[i];
+  if (KIND != KIND_GENERAL) {
+    // Diagonal fast path for all U pairs at once: n0 = cmul(q11, a0) (a0 itself for
+    // a phase), n1 = cmul(q22, a1); exact whenever no component is zero (see
+    // pair_update).  One thread-level branch per gate takes the full mix() from the
+    // untouched inputs in the rare case that one is.
+    double2 n0[U], n1[U];
+    bool act[U], bad = false;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      act[u] = !cm || (idx[u] & cm);
+      n0[u] = KIND == KIND_PHASE ? x0[u] : cmul(q[0], q[1], x0[u]);
+      n1[u] = cmul(q[6], q[7], x1[u]);
+      bad |= act[u] & !(nonzero2(n0[u]) & nonzero2(n1[u]));
+    }
+    if (bad) {
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (act[u]) pair_update<KIND_GENERAL>(x0[u], x1[u], q);
+    } else {
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (act[u]) {
+          x0[u] = n0[u];
+          x1[u] = n1[u];
+        }
+    }
+    return;
+  }
+  if (!cm) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) pair_update<KIND>(x0[u], x1[u], q);
+    return;
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    if (!(idx[u] & cm)) continue;
+    pair_update<KIND>(x0[u], x1[u], q);
+  }
+}
+
+template <int U>
+__device__ __forceinline__ void stage_apply(double2 (&x0)[U], double2 (&x1)[U], const uint64_t (&idx)[U],
+                                            const StageParams &P) {
+  for (int gi = 0; gi < P.ngates; ++gi) {
+    const StageGate &G = P.g[gi];
+    const uint64_t cm = G.control >= 0 ? (1ull << G.control) : 0ull;
+    if (G.kind == KIND_PHASE)
+      stage_gate<KIND_PHASE, U>(x0, x1, idx, cm, G.q);
+    else if (G.kind == KIND_DIAG)
+      stage_gate<KIND_DIAG, U>(x0, x1, idx, cm, G.q);
+    else
+      stage_gate<KIND_GENERAL, U>(x0, x1, idx, cm, G.q);
+  }
+}
+
 __global__ void __launch_bounds__(BLK) k_stage_pairs(double2 *__restrict__ a, uint64_t npairs, int t,
                                                      const StageParams P) {
   const uint64_t tb = 1ull << t;
-  const uint64_t p0 = (uint64_t)blockIdx.x * (BLK * UNROLL) + threadIdx.x;
-  double2 x0[UNROLL], x1[UNROLL];
-  uint64_t i0[UNROLL];
+  const uint64_t p0 = (uint64_t)blockIdx.x * (BLK * SUNROLL) + threadIdx.x;
+  double2 x0[SUNROLL], x1[SUNROLL];
+  uint64_t i0[SUNROLL];
 #pragma unroll
-  for (int u = 0; u < UNROLL; ++u) {
+  for (int u = 0; u < SUNROLL; ++u) {
     const uint64_t p = p0 + (uint64_t)u * BLK;
     i0[u] = insert_zero(p, t);
     if (p < npairs) {
@@ -437,16 +567,9 @@ __global__ void __launch_bounds__(BLK) k_stage_pairs(double2 *__restrict__ a, ui
       x1[u] = a[i0[u] | tb];
     }
   }
-  for (int gi = 0; gi < P.ngates; ++gi) {
-    const StageGate &G = P.g[gi];
+  stage_apply<SUNROLL>(x0, x1, i0, P);
 #pragma unroll
-    for (int u = 0; u < UNROLL; ++u) {
-      if (G.control >= 0 && !((i0[u] >> G.control) & 1ull)) continue;
-      pair_update_kind(G.kind, x0[u], x1[u], G.q);
-    }
-  }
-#pragma unroll
-  for (int u = 0; u < UNROLL; ++u) {
+  for (int u = 0; u < SUNROLL; ++u) {
     const uint64_t p = p0 + (uint64_t)u * BLK;
     if (p >= npairs) continue;
     a[i0[u]] = x0[u];
@@ -518,14 +641,7 @@ __global__ void __launch_bounds__(BLK) k_exchange_stage(double2 *__restrict__ mi
       x1[u] = own_is_zero ? at : am;
     }
   }
-  for (int gi = 0; gi < P.ngates; ++gi) {
-    const StageGate &G = P.g[gi];
-#pragma unroll
-    for (int u = 0; u < UNROLL; ++u) {
-      if (G.control >= 0 && !((jj[u] >> G.control) & 1ull)) continue;
-      pair_update_kind(G.kind, x0[u], x1[u], G.q);
-    }
-  }
+  stage_apply<UNROLL>(x0, x1, jj, P);
 #pragma unroll
   for (int u = 0; u < UNROLL; ++u) {
     const uint64_t p = p0 + (uint64_t)u * BLK;
@@ -808,7 +924,7 @@ int run_stage(double2 *a, int m, const sv_gate *gates, int n, cudaStream_t st) {
     memcpy(P.g[i].q, gates[i].q, sizeof(P.g[i].q));
   }
   const uint64_t np = 1ull << (m - 1);
-  k_stage_pairs<<<grid_for(np, BLK * UNROLL), BLK, 0, st>>>(a, np, t, P);
+  k_stage_pairs<<<grid_for(np, BLK * SUNROLL), BLK, 0, st>>>(a, np, t, P);
   return after_launch("k_stage_pairs");
 }
 

@@ -67,10 +67,26 @@ def main():
                 ms = timeit(lambda: sv.run_fused(st, gates, lmax), a.reps)
                 emit(kind="fused", gates=G, lmax=lmax, ms=round(ms, 4), phys_gbps=round((32 << n) / ms / 1e6, 1),
                      eff_gbps=round(G * (32 << n) / ms / 1e6, 1))
+    if "tile" in what:
+        for G in (1, 4, 16, 64):
+            for T in (12, 13):
+                gates = [sv.GateOp(sv.random_unitary(rng), int(rng.integers(T))) for _ in range(G)]
+                ms = timeit(lambda: sv.kernels.apply_gates(st.amps, gates, tile=T), a.reps)
+                emit(kind="tile", gates=G, T=T, ms=round(ms, 4), phys_gbps=round((32 << n) / ms / 1e6, 1),
+                     eff_gbps=round(G * (32 << n) / ms / 1e6, 1))
+        for k in (13, 20, n - 1):
+            for G in (2, 8, 30):
+                gates = [sv.GateOp(sv.hadamard(), k)] + [sv.GateOp(sv.phase_r(j + 2), k, (k + 1 + j) % n)
+                                                          for j in range(G - 1)]
+                ms = timeit(lambda: sv.kernels.apply_gates(st.amps, gates), a.reps)
+                emit(kind="stage", k=k, gates=G, ms=round(ms, 4), phys_gbps=round((32 << n) / ms / 1e6, 1))
     if "qft" in what:
         circ = sv.build_qft(n)
-        for l_c in (None, 12, 13):
-            fusion = None if l_c is None else sv.FusionConfig(l_c=l_c)
+        for l_c in (None, 12, 13, "p12", "p13"):
+            if isinstance(l_c, str):
+                fusion = sv.FusionConfig(l_c=int(l_c[1:]), passes=True)
+            else:
+                fusion = None if l_c is None else sv.FusionConfig(l_c=l_c)
             ms = timeit(lambda: sv.run_circuit(st, circ, fusion=fusion), max(1, a.reps // 2))
             eff = sum((32 if op.control is None else 16) << n for op in circ)
             emit(kind="qft", n=n, l_c=l_c, gates=len(circ), ms=round(ms, 3), eff_gbps=round(eff / ms / 1e6, 1),
@@ -79,8 +95,11 @@ def main():
         m = 20
         s20 = sv.init_random_state(sv.Layout(m), seed=2)
         circ = sv.random_circuit(m, 200, np.random.default_rng(1), controlled_fraction=0.0)
-        for l_c in (None, 12, 13):
-            fusion = None if l_c is None else sv.FusionConfig(l_c=l_c)
+        for l_c in (None, 12, 13, "p13"):
+            if isinstance(l_c, str):
+                fusion = sv.FusionConfig(l_c=int(l_c[1:]), passes=True)
+            else:
+                fusion = None if l_c is None else sv.FusionConfig(l_c=l_c)
             ms = timeit(lambda: sv.run_circuit(s20, circ, fusion=fusion), a.reps)
             emit(kind="config1", n=m, l_c=l_c, gates=200, ms=round(ms, 3), us_per_gate=round(ms * 1e3 / 200, 2),
                  eff_gbps=round(200 * (32 << m) / ms / 1e6, 1))
