@@ -491,67 +491,82 @@ struct StageParams {
 
 constexpr int SUNROLL = 4;
 
+// One gate of a stage on U register pairs.  ok0[u] caches nonzero2(x0[u]):
+// a phase gate leaves x0 untouched on its fast path, so a stage of phases
+// tests each x0 once instead of once per gate.  Inactive pairs (control bit
+// clear) cost one test and a branch (warp-uniform unless the control is one
+// of the five lowest pair-index bits).
 template <int KIND, int U>
-__device__ __forceinline__ void stage_gate(double2 (&x0)[U], double2 (&x1)[U], const uint64_t (&idx)[U],
-                                           uint64_t cm, const double *qp) {
+__device__ __forceinline__ void stage_gate(double2 (&x0)[U], double2 (&x1)[U], bool (&ok0)[U],
+                                           const uint64_t (&idx)[U], uint64_t cm, const double *qp) {
   double q[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) q[i] = qp[i];
-  if (KIND != KIND_GENERAL) {
-    // Diagonal fast path for all U pairs at once: n0 = cmul(q11, a0) (a0 itself for
-    // a phase), n1 = cmul(q22, a1); exact whenever no component is zero (see
-    // pair_update).  One thread-level branch per gate takes the full mix() from the
-    // untouched inputs in the rare case that one is.
-    double2 n0[U], n1[U];
-    bool act[U], bad = false;
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      act[u] = !cm || (idx[u] & cm);
-      n0[u] = KIND == KIND_PHASE ? x0[u] : cmul(q[0], q[1], x0[u]);
-      n1[u] = cmul(q[6], q[7], x1[u]);
-      bad |= act[u] & !(nonzero2(n0[u]) & nonzero2(n1[u]));
-    }
-    if (bad) {
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (act[u]) pair_update<KIND_GENERAL>(x0[u], x1[u], q);
-    } else {
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (act[u]) {
-          x0[u] = n0[u];
-          x1[u] = n1[u];
-        }
-    }
-    return;
-  }
-  if (!cm) {
-#pragma unroll
-    for (int u = 0; u < U; ++u) pair_update<KIND>(x0[u], x1[u], q);
-    return;
-  }
 #pragma unroll
   for (int u = 0; u < U; ++u) {
-    if (!(idx[u] & cm)) continue;
-    pair_update<KIND>(x0[u], x1[u], q);
+    if (cm && !(idx[u] & cm)) continue;
+    if (KIND == KIND_GENERAL) {
+      pair_update<KIND_GENERAL>(x0[u], x1[u], q);
+      ok0[u] = nonzero2(x0[u]);
+      continue;
+    }
+    const double2 n1 = cmul(q[6], q[7], x1[u]);
+    if (KIND == KIND_PHASE) {
+      if (__builtin_expect(ok0[u] & nonzero2(n1), 1)) {
+        x1[u] = n1;
+        continue;
+      }
+    } else {
+      const double2 n0 = cmul(q[0], q[1], x0[u]);
+      if (__builtin_expect(nonzero2(n0) & nonzero2(n1), 1)) {
+        x0[u] = n0;
+        x1[u] = n1;
+        ok0[u] = true;
+        continue;
+      }
+    }
+    pair_update<KIND_GENERAL>(x0[u], x1[u], q);  // exact: the definition itself
+    ok0[u] = nonzero2(x0[u]);
   }
 }
 
-template <int U>
-__device__ __forceinline__ void stage_apply(double2 (&x0)[U], double2 (&x1)[U], const uint64_t (&idx)[U],
-                                            const StageParams &P) {
-  for (int gi = 0; gi < P.ngates; ++gi) {
+__device__ __forceinline__ void stage_gate_any(int kind, double2 (&x0)[SUNROLL], double2 (&x1)[SUNROLL],
+                                               bool (&ok0)[SUNROLL], const uint64_t (&idx)[SUNROLL], uint64_t cm,
+                                               const double *q) {
+  if (kind == KIND_PHASE)
+    stage_gate<KIND_PHASE, SUNROLL>(x0, x1, ok0, idx, cm, q);
+  else if (kind == KIND_DIAG)
+    stage_gate<KIND_DIAG, SUNROLL>(x0, x1, ok0, idx, cm, q);
+  else
+    stage_gate<KIND_GENERAL, SUNROLL>(x0, x1, ok0, idx, cm, q);
+}
+
+// SIG 0: any mix of kinds.  SIG 1: gate 0 of any kind, every later gate a phase
+// (a transform stage H(k), R(k, c)...): the gate loop then has no kind branch,
+// so no register shuffling between branch variants.
+template <int SIG>
+__device__ __forceinline__ void stage_apply(double2 (&x0)[SUNROLL], double2 (&x1)[SUNROLL],
+                                            const uint64_t (&idx)[SUNROLL], const StageParams &P) {
+  bool ok0[SUNROLL];
+#pragma unroll
+  for (int u = 0; u < SUNROLL; ++u) ok0[u] = nonzero2(x0[u]);
+  int gi = 0;
+  if (SIG == 1) {
+    const StageGate &G = P.g[0];
+    stage_gate_any(G.kind, x0, x1, ok0, idx, G.control >= 0 ? (1ull << G.control) : 0ull, G.q);
+    for (gi = 1; gi < P.ngates; ++gi) {
+      const StageGate &H = P.g[gi];
+      stage_gate<KIND_PHASE, SUNROLL>(x0, x1, ok0, idx, H.control >= 0 ? (1ull << H.control) : 0ull, H.q);
+    }
+    return;
+  }
+  for (; gi < P.ngates; ++gi) {
     const StageGate &G = P.g[gi];
-    const uint64_t cm = G.control >= 0 ? (1ull << G.control) : 0ull;
-    if (G.kind == KIND_PHASE)
-      stage_gate<KIND_PHASE, U>(x0, x1, idx, cm, G.q);
-    else if (G.kind == KIND_DIAG)
-      stage_gate<KIND_DIAG, U>(x0, x1, idx, cm, G.q);
-    else
-      stage_gate<KIND_GENERAL, U>(x0, x1, idx, cm, G.q);
+    stage_gate_any(G.kind, x0, x1, ok0, idx, G.control >= 0 ? (1ull << G.control) : 0ull, G.q);
   }
 }
 
+template <int SIG>
 __global__ void __launch_bounds__(BLK) k_stage_pairs(double2 *__restrict__ a, uint64_t npairs, int t,
                                                      const StageParams P) {
   const uint64_t tb = 1ull << t;
@@ -567,7 +582,7 @@ __global__ void __launch_bounds__(BLK) k_stage_pairs(double2 *__restrict__ a, ui
       x1[u] = a[i0[u] | tb];
     }
   }
-  stage_apply<SUNROLL>(x0, x1, i0, P);
+  stage_apply<SIG>(x0, x1, i0, P);
 #pragma unroll
   for (int u = 0; u < SUNROLL; ++u) {
     const uint64_t p = p0 + (uint64_t)u * BLK;
@@ -625,6 +640,7 @@ __global__ void __launch_bounds__(BLK) k_exchange(double2 *__restrict__ mine, do
 // pair crosses NVLink once each way however many gates the stage holds
 // (controls: local bits -> per-element predicate; rank bits were resolved on
 // the host, both partners see the same list).
+template <int SIG>
 __global__ void __launch_bounds__(BLK) k_exchange_stage(double2 *__restrict__ mine, double2 *__restrict__ theirs,
                                                         uint64_t count, uint64_t base, int own_is_zero,
                                                         const StageParams P) {
@@ -641,7 +657,7 @@ __global__ void __launch_bounds__(BLK) k_exchange_stage(double2 *__restrict__ mi
       x1[u] = own_is_zero ? at : am;
     }
   }
-  stage_apply<UNROLL>(x0, x1, jj, P);
+  stage_apply<SIG>(x0, x1, jj, P);
 #pragma unroll
   for (int u = 0; u < UNROLL; ++u) {
     const uint64_t p = p0 + (uint64_t)u * BLK;
@@ -914,6 +930,12 @@ int launch_gate(double2 *a, int m, const sv_gate &g, cudaStream_t st) {
   return launch_local<MODE_CTL>(a, m - 1, tv, g.control, q, st, "controlled");
 }
 
+int stage_sig(const StageParams &P) {
+  for (int i = 1; i < P.ngates; ++i)
+    if (P.g[i].kind != KIND_PHASE) return 0;
+  return 1;
+}
+
 int run_stage(double2 *a, int m, const sv_gate *gates, int n, cudaStream_t st) {
   static thread_local StageParams P;
   const int t = gates[0].target;
@@ -924,7 +946,10 @@ int run_stage(double2 *a, int m, const sv_gate *gates, int n, cudaStream_t st) {
     memcpy(P.g[i].q, gates[i].q, sizeof(P.g[i].q));
   }
   const uint64_t np = 1ull << (m - 1);
-  k_stage_pairs<<<grid_for(np, BLK * SUNROLL), BLK, 0, st>>>(a, np, t, P);
+  if (stage_sig(P) == 1)
+    k_stage_pairs<1><<<grid_for(np, BLK * SUNROLL), BLK, 0, st>>>(a, np, t, P);
+  else
+    k_stage_pairs<0><<<grid_for(np, BLK * SUNROLL), BLK, 0, st>>>(a, np, t, P);
   return after_launch("k_stage_pairs");
 }
 
@@ -1064,8 +1089,13 @@ int sv_exchange_stage(void *mine, void *theirs, int m, int own_is_zero, const sv
     memcpy(P.g[i].q, gates[i].q, sizeof(P.g[i].q));
   }
   const uint64_t half = 1ull << (m - 1);
-  k_exchange_stage<<<grid_for(half, BLK * UNROLL), BLK, 0, (cudaStream_t)stream>>>(
-      (double2 *)mine, (double2 *)theirs, half, own_is_zero ? 0 : half, own_is_zero ? 1 : 0, P);
+  const unsigned grid = grid_for(half, BLK * SUNROLL);
+  if (stage_sig(P) == 1)
+    k_exchange_stage<1><<<grid, BLK, 0, (cudaStream_t)stream>>>((double2 *)mine, (double2 *)theirs, half,
+                                                                own_is_zero ? 0 : half, own_is_zero ? 1 : 0, P);
+  else
+    k_exchange_stage<0><<<grid, BLK, 0, (cudaStream_t)stream>>>((double2 *)mine, (double2 *)theirs, half,
+                                                                own_is_zero ? 0 : half, own_is_zero ? 1 : 0, P);
   return after_launch("sv_exchange_stage");
 }
 
