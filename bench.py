@@ -44,6 +44,10 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=["sweep", "controlled", "random", "qft"], default="sweep")
     ap.add_argument("--n", type=int, default=None, help="total qubits (default 30 + log2(N))")
+    ap.add_argument("--fusion", choices=["none", "passes"], default=None,
+                    help="none: one launch per gate (default, BASELINE config 2 is per-gate); "
+                         "passes: native pass planner (default for --workload qft)")
+    ap.add_argument("--l-c", type=int, default=12, help="register tile exponent for --fusion passes")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
@@ -72,6 +76,14 @@ def step_circuits(sv, workload, n, count, seed=1):
         else:
             out.append(sv.build_qft(n))
     return out
+
+
+WORKLOADS = {
+    "sweep": "BASELINE config 2: n={n}, one fresh Haar gate per target k=0..{n1} per step",
+    "controlled": "BASELINE config 3 shape: n={n}, 30 Haar controlled gates per step, (c,t) uniform distinct",
+    "random": "BASELINE config 4 shape: n={n}, 25 Haar single-qubit gates per step, targets uniform",
+    "qft": "BASELINE config 5 shape: transform circuit build_qft(n={n}) per step",
+}
 
 
 def effective_bytes(circ, n):
@@ -213,6 +225,40 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def make_units(sv, circ, m, fusion, l_c, state, fabric):
+    """The launch groups of one step: (kind, algorithmic HBM bytes, gate count, callable).
+
+    Unfused: one unit per gate (the reference's engine.py:88-95 loop).  Passes:
+    one unit per HBM pass of the native planner (passes.py)."""
+    if fusion == "passes":
+        from paper_1601_07195_b200.passes import tile_for
+
+        tile = tile_for(l_c, m)
+        return [("pass-" + p.kind, 32 << m, len(p.gates),
+                 (lambda p=p: sv.execute_pass(state, p, fabric, tile=tile)))
+                for p in sv.plan_passes(circ.gates, m, tile)]
+    units = []
+    for op in circ:
+        case = sv.classify_case(op.target, op.control, m)
+        if case in (sv.BoundCase.SINGLE_LOCAL, sv.BoundCase.CONTROLLED_REMOTE_CONTROL):
+            kind, nbytes = "single", 32 << m
+        elif case is sv.BoundCase.CONTROLLED_LOCAL:
+            kind, nbytes = "controlled", 16 << m
+        else:
+            kind, nbytes = "exchange", sv.link_bytes_per_direction(case, m)
+        units.append((kind, nbytes, 1, (lambda op=op: sv.apply_op(state, op, fabric))))
+    return units
+
+
+KERNELS = {
+    "single": ("sv_apply_single", "k_pairs/k_shfl<MODE_SINGLE> (sv_apply_single)"),
+    "controlled": ("sv_apply_controlled", "k_pairs/k_shfl<MODE_CTL|MODE_PRED> (sv_apply_controlled)"),
+    "pass-local_stage": ("sv_apply_gates:stage", "k_stage_pairs (sv_apply_gates, same-target stage pass)"),
+    "pass-local_tile": ("sv_apply_gates:tile", "k_tile (sv_apply_gates, register-tiled run)"),
+    "pass-local_gate": ("sv_apply_single", "k_pairs/k_shfl (single gate of a pass plan)"),
+}
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -236,9 +282,11 @@ def main():
     n = args.n or (30 + g)
     lay = sv.Layout(n, g, rank)
     m = lay.m
+    fusion = args.fusion or ("passes" if args.workload == "qft" else "none")
     circs = step_circuits(sv, args.workload, n, args.warmup + args.steps)
     state = sv.init_random_state(lay, seed=0, transport=fabric, device=dev)
     stream = torch.cuda.current_stream()
+    fcfg = sv.FusionConfig(l_c=args.l_c, passes=True) if fusion == "passes" else None
 
     def barrier():
         torch.cuda.synchronize()
@@ -247,11 +295,13 @@ def main():
 
     # ---------------------------------------------------------- warm-up
     for c in circs[: args.warmup]:
-        sv.run_circuit(state, c, fabric)
+        for _, _, _, fn in make_units(sv, c, m, fusion, args.l_c, state, fabric):
+            fn()
     barrier()
 
     # ------------------------------------------------ timed (device-resident)
     timed = circs[args.warmup:]
+    units = [make_units(sv, c, m, fusion, args.l_c, state, fabric) for c in timed]
     ev = []
     launches0 = sv.launch_count()
     with ClockSampler(local) as clocks:
@@ -259,11 +309,11 @@ def main():
         t_start = torch.cuda.Event(enable_timing=True)
         t_end = torch.cuda.Event(enable_timing=True)
         t_start.record(stream)
-        for c in timed:
+        for us in units:
             row = [torch.cuda.Event(enable_timing=True)]
             row[0].record(stream)
-            for op in c:
-                sv.apply_op(state, op, fabric)
+            for _, _, _, fn in us:
+                fn()
                 e = torch.cuda.Event(enable_timing=True)
                 e.record(stream)
                 row.append(e)
@@ -277,55 +327,63 @@ def main():
         dist.all_reduce(t[:1], op=dist.ReduceOp.MAX)
         dist.all_reduce(t[1:], op=dist.ReduceOp.SUM)
         elapsed_ms, launches = float(t[0]), int(t[1])
-    gate_ms = np.array([[row[i].elapsed_time(row[i + 1]) for i in range(len(row) - 1)] for row in ev])
+    unit_ms = [[row[i].elapsed_time(row[i + 1]) for i in range(len(row) - 1)] for row in ev]
     ngates = sum(len(c) for c in timed)
     eff = sum(effective_bytes(c, n) for c in timed)
     value = eff / (elapsed_ms * 1e-3) / 1e9
 
-    # roofline of the dominant kernel: local single-qubit update (sv_apply_single)
+    # roofline of the dominant local kernel (largest share of the step)
     peaks, peak_kind = load_peaks()
-    local_single = [(j, i) for j, c in enumerate(timed) for i, op in enumerate(c)
-                    if op.control is None and op.target < m]
-    per_target = {}
+    by_kind: dict = {}
+    for us, ms in zip(units, unit_ms):
+        for (kind, nbytes, cnt, _), t_ms in zip(us, ms):
+            by_kind.setdefault(kind, []).append((nbytes, t_ms, cnt))
+    local_kinds = [k for k in by_kind if k in KERNELS]
     roof = None
-    if local_single:
-        d = np.array([gate_ms[j][i] for j, i in local_single])
-        avg_ms = float(d.mean())
-        achieved = (32 << m) / (avg_ms * 1e-3) / 1e9
+    if local_kinds:
+        top = max(local_kinds, key=lambda k: sum(t for _, t, _ in by_kind[k]))
+        rows = by_kind[top]
+        avg_ms = float(np.mean([t for _, t, _ in rows]))
+        alg = int(np.mean([b for b, _, _ in rows]))
+        achieved = alg / (avg_ms * 1e-3) / 1e9
+        key, kname = KERNELS[top]
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": ncu_traffic("sv_apply_single", 32 << m),
-                "kernel": "k_pairs/k_shfl<MODE_SINGLE> (sv_apply_single)", "peak_kind": peak_kind,
-                "algorithmic_bytes_per_launch": 32 << m, "avg_launch_ms": round(avg_ms, 4),
+                "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": ncu_traffic(key, alg),
+                "kernel": kname, "peak_kind": peak_kind, "algorithmic_bytes_per_launch": alg,
+                "avg_launch_ms": round(avg_ms, 4), "launches": len(rows),
+                "share_of_step": round(sum(t for _, t, _ in rows) / elapsed_ms, 4),
                 "frac_of_8TBs": round(achieved / 8000.0, 4)}
-        if args.workload == "sweep":
-            for k in range(m):
-                ks = [gate_ms[j][k] for j in range(len(timed))]
-                per_target[k] = round((32 << m) / (float(np.median(ks)) * 1e-3) / 1e9, 1)
+        if top.startswith("pass-"):
+            roof["gates_per_launch"] = round(float(np.mean([c for _, _, c in rows])), 2)
+    per_target = {}
+    if args.workload == "sweep" and fusion == "none":
+        for k in range(m):
+            ks = [unit_ms[j][k] for j in range(len(timed))]
+            per_target[k] = round((32 << m) / (float(np.median(ks)) * 1e-3) / 1e9, 1)
     nvlink = None
-    if world > 1:
-        glob = [(j, i) for j, c in enumerate(timed) for i, op in enumerate(c) if op.max_qubit() >= m]
-        if glob:
-            d = np.array([gate_ms[j][i] for j, i in glob])
-            per_dir = 1 << (m + 4)
-            nvlink = {"achieved_gbs_per_direction": round(per_dir / (float(d.mean()) * 1e-3) / 1e9, 1),
-                      "peak_nominal": 900.0, "peak_measured_ref": 770.0,
-                      "frac_nominal": round(per_dir / (float(d.mean()) * 1e-3) / 1e9 / 900.0, 4),
-                      "global_gates_per_step": len(glob) // len(timed), "avg_gate_ms": round(float(d.mean()), 3)}
+    glob = [r for k, rs in by_kind.items() if k in ("exchange", "pass-global_stage", "pass-global_gate") for r in rs]
+    if world > 1 and glob:
+        per_dir = 1 << (m + 4)
+        d = float(np.mean([t for _, t, _ in glob]))
+        nvlink = {"achieved_gbs_per_direction": round(per_dir / (d * 1e-3) / 1e9, 1),
+                  "peak_nominal": 900.0, "peak_measured_ref": 770.0,
+                  "frac_nominal": round(per_dir / (d * 1e-3) / 1e9 / 900.0, 4),
+                  "global_launches_per_step": len(glob) // len(timed), "avg_ms": round(d, 3)}
 
     # ---------------------------------------------- end to end (host buffers)
     e2e = None
     cpu = None
     if not args.no_e2e:
-        host = torch.empty(lay.local_len, dtype=torch.complex128, pin_memory=True)
-        state.store_host(host)
+        h_in = torch.empty(lay.local_len, dtype=torch.complex128, pin_memory=True)
+        h_out = torch.empty(lay.local_len, dtype=torch.complex128, pin_memory=True)
+        state.store_host(h_in)
         barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        for c in timed:
-            state.load_host(host)                 # H2D of the step's input state
-            sv.run_circuit(state, c, fabric)
-            state.store_host(host)                # D2H of the step's result
+        # every step: pinned H2D of its input, the circuit, D2H of its result; the
+        # public run_pipelined overlaps step i+1's upload / step i-1's download with step i
+        sv.run_pipelined(lay, timed, [h_in] * len(timed), [h_out] * len(timed), fabric, fusion=fcfg)
         e1.record(stream)
         torch.cuda.synchronize()
         e2e_ms = e0.elapsed_time(e1)
@@ -336,10 +394,11 @@ def main():
         e2e = {"value": round(eff / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
                "h2d_bytes_per_step": (16 << m) * world, "d2h_bytes_per_step": (16 << m) * world,
                "ms_per_step": round(e2e_ms / len(timed), 3),
-               "path": "LocalState.load_host -> run_circuit -> LocalState.store_host (sv_copy + kernels)"}
+               "path": "run_pipelined: LocalState.load_host (sv_copy, H2D stream) -> run_circuit -> "
+                       "LocalState.store_host (sv_copy, D2H stream), two device slots"}
         if rank == 0 and world == 1 and not args.no_cpu_baseline:
-            cpu = cpu_baseline(sv, host, n, timed[0], args.cpu_seconds)
-        del host
+            cpu = cpu_baseline(sv, h_in, n, timed[0], args.cpu_seconds)
+        del h_in, h_out
 
     if rank == 0:
         line = {
@@ -347,11 +406,12 @@ def main():
             "warmup": args.warmup, "ms_per_step": round(elapsed_ms / args.steps, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
             "gates_per_s": round(ngates / (elapsed_ms * 1e-3), 3),
-            "config": {"workload": f"{args.workload}: n={n}, one fresh Haar gate per target k=0..{n - 1} per step"
-                       if args.workload == "sweep" else f"{args.workload}: n={n}",
+            "config": {"workload": WORKLOADS[args.workload].format(n=n, n1=n - 1),
+                       "fusion": fusion if fusion == "none" else f"{fusion} (l_c={args.l_c})",
                        "n_qubits": n, "local_qubits": m, "global_qubits": g, "gates_per_step": len(timed[0]),
                        "state_gib_per_gpu": (16 << m) / 2**30, "parallelism": f"state sharded over {world} GPU(s)",
-                       "l2": "no flush: 16 GiB slice >> 126 MB L2", "seed": {"state": 0, "circuit": 1}},
+                       "l2": "no flush: slice >> 126 MB L2" if m >= 26 else "slice fits L2 (parity-size run)",
+                       "seed": {"state": 0, "circuit": 1}},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks.summary(),
         }

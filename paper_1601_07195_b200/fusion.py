@@ -143,7 +143,7 @@ def execute_plan(state: LocalState, plan: FusionPlan, policy: ThreadPolicy = SER
         from .passes import execute_pass, plan_passes, tile_for
 
         tile = tile_for(plan.l_c, state.layout.m)
-        for p in plan_passes(plan.flatten(), state.layout.m):
+        for p in plan_passes(plan.flatten(), state.layout.m, tile):
             execute_pass(state, p, transport, tile=tile)
         return
     if plan.l_c > state.layout.m:

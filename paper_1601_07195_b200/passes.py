@@ -32,29 +32,49 @@ from .errors import LayoutError
 from .kernels import _as_gate
 
 
+LOCAL_KINDS = ("local_tile", "local_stage", "local_gate")
+
+
 @dataclass(frozen=True)
 class Pass:
-    kind: str                # "local" | "global_stage" | "global_gate"
+    kind: str                # local_tile | local_stage | local_gate | global_stage | global_gate
     gates: tuple[GateOp, ...]
     target: int | None = None
 
+    @property
+    def local(self) -> bool:
+        return self.kind in LOCAL_KINDS
 
-def plan_passes(gates, m: int) -> list[Pass]:
-    """Cut a gate sequence into passes (pure function of the gates and m: identical on every rank)."""
+
+def plan_passes(gates, m: int, tile: int = 0) -> list[Pass]:
+    """Cut a gate sequence into HBM passes -- a pure function of the gates, m and the tile,
+    so every rank derives the same list (the collective fences line up).
+
+    Local targets: a maximal run of targets below the register tile is one
+    ``local_tile`` pass; a maximal run sharing one higher target is one
+    ``local_stage`` pass; a lone gate is a ``local_gate``.  Global targets: a
+    run sharing the target is one ``global_stage`` exchange.  This is the
+    grouping ``sv_apply_gates`` applies natively, exposed so each pass can be
+    timed and recorded on its own."""
     gates = list(gates)
+    T = tile if tile else min(m, _lib.SV_FUSED_MAX_TILE)
     out: list[Pass] = []
     i, n = 0, len(gates)
     while i < n:
         t = gates[i].target
         j = i + 1
-        if t < m:
-            while j < n and gates[j].target < m:
-                j += 1
-            out.append(Pass("local", tuple(gates[i:j])))
-        else:
+        if t >= m:
             while j < n and gates[j].target == t and j - i < _lib.SV_STAGE_MAX_GATES:
                 j += 1
             out.append(Pass("global_stage" if j - i > 1 else "global_gate", tuple(gates[i:j]), t))
+        elif T >= 9 and t < T:
+            while j < n and gates[j].target < T:
+                j += 1
+            out.append(Pass("local_tile" if j - i > 1 else "local_gate", tuple(gates[i:j]), t))
+        else:
+            while j < n and gates[j].target == t and j - i < _lib.SV_STAGE_MAX_GATES:
+                j += 1
+            out.append(Pass("local_stage" if (j - i > 1 and t >= 5) else "local_gate", tuple(gates[i:j]), t))
         i = j
     return out
 
@@ -75,7 +95,7 @@ def _resolve_rank_controls(ops, layout) -> list[GateOp]:
 def execute_pass(state, p: Pass, transport=None, *, tile: int = 0, executor=None) -> None:
     lay = state.layout
     ex = executor or (transport.executor if transport is not None else _CUDA)
-    if p.kind == "local":
+    if p.local:
         ops = _resolve_rank_controls(p.gates, lay)
         if ops:
             ex.local_gates(state, ops, tile)
