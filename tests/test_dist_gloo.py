@@ -53,6 +53,17 @@ class ShmOracleExecutor:
 
         oracle.exchange_raw(state.amps.ctypes.data, theirs, state.layout.m, own_is_zero, c_local, q.mat)
 
+    def exchange_stage(self, state, theirs, own_is_zero, ops):
+        # a same-target stage == its gates' exchanges in order (each keeps the half split)
+        for op in ops:
+            self.exchange(state, theirs, own_is_zero, -1 if op.control is None else op.control, op.gate)
+
+    def local_gates(self, state, ops, tile=0):
+        from oracle import oracle
+
+        for op in ops:
+            oracle.apply_gate(state.amps, (op.target, op.control, op.gate.mat))
+
     def synchronize(self, state):
         pass
 
@@ -157,3 +168,74 @@ def test_gloo_world_matches_reference(golden, world, name, n):
     assert int(out["tags"]) == glob            # one fresh tag per global-qubit gate, on every rank
     fenced = sum(1 for t, c, _ in unpack_ops(d, name) if t >= m)
     assert int(out["fences"]) == 2 * fenced + 2  # two fences per exchange-class gate + two final barriers
+
+
+def _worker_passes(rank, world, port, path, n):
+    """Pass-fused execution (FusionConfig(passes=True) semantics): global stages exchange once."""
+    import torch.distributed as dist
+
+    import paper_1601_07195_b200 as sv
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        p = world.bit_length() - 1
+        d = dict(np.load(path + ".npz"))
+        lay = sv.Layout(n, p, rank)
+        m = lay.m
+        shm = shared_memory.SharedMemory(create=True, size=16 << m, name=f"svp_{os.getpid()}_{rank}")
+        amps = np.ndarray((1 << m,), dtype=np.complex128, buffer=shm.buf)
+        amps[:] = d["init"][rank << m:(rank + 1) << m]
+        state = ShmState(lay, amps, shm)
+        ex = ShmOracleExecutor()
+        fabric = sv.NvlinkFabric(fence="host", executor=ex)
+        ops = [sv.GateOp(sv.GateMatrix.unchecked(q.reshape(2, 2)), int(t), None if c < 0 else int(c))
+               for t, c, q in zip(d["t"], d["c"], d["q"])]
+        plan = sv.plan_passes(ops, m, 0)
+        for pz in plan:
+            sv.execute_pass(state, pz, fabric)
+        fabric.barrier()
+        pids = fabric.exchange_objects(os.getpid())
+        if rank == 0:
+            parts = [amps.copy()]
+            for r in range(1, world):
+                other = shared_memory.SharedMemory(name=f"svp_{pids[r]}_{r}")
+                parts.append(np.ndarray((1 << m,), dtype=np.complex128, buffer=other.buf).copy())
+                other.close()
+            np.savez(path + ".out.npz", full=np.concatenate(parts), nglobal=sum(not q.local for q in plan),
+                     sent=fabric.sent_bytes)
+        fabric.barrier()
+        fabric.close()
+        del amps
+        shm.close()
+        shm.unlink()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n", [(2, 9), (4, 10)])
+def test_gloo_pass_fusion_matches_oracle(world, n):
+    """QFT + random gates through plan_passes/execute_pass: global transform stages run as one
+    exchange each (tags/fences/counters per stage) and the gathered state equals the oracle's."""
+    import torch.multiprocessing as mp
+
+    import paper_1601_07195_b200 as sv
+    from conftest import random_state
+    from oracle import oracle
+
+    rng = np.random.default_rng(world * 100 + n)
+    circ = sv.build_qft(n)
+    circ.extend(sv.random_circuit(n, 40, rng, controlled_fraction=0.5).gates)
+    init = random_state(rng, n)
+    want = init.copy()
+    oracle.run_circuit(want, circ.gates)
+    with tempfile.TemporaryDirectory() as tmp:
+        path = os.path.join(tmp, "w")
+        np.savez(path + ".npz", init=init, t=np.array([o.target for o in circ]),
+                 c=np.array([-1 if o.control is None else o.control for o in circ]),
+                 q=np.stack([o.gate.mat.reshape(4) for o in circ]))
+        mp.spawn(_worker_passes, args=(world, _port(), path, n), nprocs=world, join=True)
+        out = dict(np.load(path + ".out.npz"))
+    assert np.array_equal(out["full"].view(np.uint64), want.view(np.uint64))
+    m = n - (world.bit_length() - 1)
+    stages = [p for p in sv.plan_passes(circ.gates, m) if p.kind == "global_stage"]
+    assert len(stages) >= world.bit_length() - 1  # one exchange per global transform stage
