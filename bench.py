@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=["sweep", "controlled", "random", "qft"], default="sweep")
-    ap.add_argument("--n", type=int, default=None, help="total qubits (default 30 + log2(N))")
+    ap.add_argument("--qubits", dest="n", type=int, default=None, help="total qubits (default 30 + log2(N))")
     ap.add_argument("--fusion", choices=["none", "passes"], default=None,
                     help="none: one launch per gate (default, BASELINE config 2 is per-gate); "
                          "passes: native pass planner (default for --workload qft)")
@@ -194,11 +194,14 @@ def run_reference(args):
 
     g = world.bit_length() - 1
     n = args.n or (30 + g)
+    m = n - g
     threads = os.cpu_count() or 1
-    amps = np.empty(1 << n, dtype=np.complex128)
+    # One host holds one rank's 2^m slice (16 GiB at the default size): the CPU
+    # path is memory-bound, so the whole job on one host runs each gate's
+    # per-rank shares back to back and whole-job GB/s equals the slice rate.
+    amps = np.empty(1 << m, dtype=np.complex128)
     oracle.fill_phase(amps, threads)
-    circs = step_circuits(sv, args.workload, n, 1)
-    pool = circs[0].gates
+    pool = [op for op in step_circuits(sv, args.workload, n, 1)[0].gates if op.max_qubit() < m]
     times, eff = [], 0
     for s in range(args.warmup + args.steps):
         op = pool[(s * 7) % len(pool)]
@@ -207,7 +210,7 @@ def run_reference(args):
         dt = time.perf_counter() - t0
         if s >= args.warmup:
             times.append(dt)
-            eff += (32 if op.control is None else 16) << n
+            eff += (32 if op.control is None else 16) << m
     tot = sum(times)
     value = eff / tot / 1e9
     line = {
@@ -215,10 +218,11 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(tot / args.steps * 1e3, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
         "gates_per_s": round(args.steps / tot, 4),
-        "config": {"workload": f"{args.workload} n={n} (BASELINE config 2 at N=1)", "n_qubits": n,
-                   "sample": "one gate of the step per timed step, target k = 7*s mod n"},
+        "config": {"workload": WORKLOADS[args.workload].format(n=n, n1=n - 1), "n_qubits": n, "local_qubits": m,
+                   "sample": f"one local gate of the step per timed step (target 7*s mod len), on one "
+                             f"2^{m}-amplitude rank slice"},
         "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": threads, "kind": "port",
-                         "sample": f"{args.steps} single gates of the n={n} sweep on a host state, "
+                         "sample": f"{args.steps} gates of the step on a 2^{m}-amplitude host slice, "
                                    f"oracle/sv_oracle.c (C restatement of kernels.py:120-196), {threads} threads"},
         "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -270,11 +274,19 @@ def main():
     import paper_1601_07195_b200 as sv
 
     world, rank, local = dist_env()
+    # SVB_SHARE_DEVICE=1 (diagnostics only): every rank on cuda:0 over gloo with host fences,
+    # to exercise the multi-rank bench path on a one-GPU box.  Never used for reported numbers.
+    shared = os.environ.get("SVB_SHARE_DEVICE") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     fabric = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
         fabric = sv.NvlinkFabric()
     if world & (world - 1):
         raise SystemExit("--gpus must be a power of two")
@@ -292,6 +304,11 @@ def main():
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
+
+    def reduce_scalar(x, op):
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if shared else dev)
+        dist.all_reduce(t, op=op)
+        return float(t[0])
 
     # ---------------------------------------------------------- warm-up
     for c in circs[: args.warmup]:
@@ -323,10 +340,8 @@ def main():
     launches = sv.launch_count() - launches0
     elapsed_ms = t_start.elapsed_time(t_end)
     if world > 1:
-        t = torch.tensor([elapsed_ms, float(launches)], dtype=torch.float64, device=dev)
-        dist.all_reduce(t[:1], op=dist.ReduceOp.MAX)
-        dist.all_reduce(t[1:], op=dist.ReduceOp.SUM)
-        elapsed_ms, launches = float(t[0]), int(t[1])
+        elapsed_ms = reduce_scalar(elapsed_ms, dist.ReduceOp.MAX)
+        launches = int(reduce_scalar(float(launches), dist.ReduceOp.SUM))
     unit_ms = [[row[i].elapsed_time(row[i + 1]) for i in range(len(row) - 1)] for row in ev]
     ngates = sum(len(c) for c in timed)
     eff = sum(effective_bytes(c, n) for c in timed)
@@ -388,9 +403,7 @@ def main():
         torch.cuda.synchronize()
         e2e_ms = e0.elapsed_time(e1)
         if world > 1:
-            t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_ms = float(t[0])
+            e2e_ms = reduce_scalar(e2e_ms, dist.ReduceOp.MAX)
         e2e = {"value": round(eff / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
                "h2d_bytes_per_step": (16 << m) * world, "d2h_bytes_per_step": (16 << m) * world,
                "ms_per_step": round(e2e_ms / len(timed), 3),

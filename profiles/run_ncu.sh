@@ -4,7 +4,7 @@
 set -e
 OUT=${OUT:-gpurun_out}
 mkdir -p $OUT
-CMD="python bench.py --n 28 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline"
+CMD="python bench.py --qubits 28 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline"
 $CMD > $OUT/ncu_plain.log 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv $CMD > $OUT/ncu_launches.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_shfl -s 60 -c 1 -o $OUT/prof_shfl $CMD > $OUT/ncu_full1.log 2>&1
