@@ -389,16 +389,26 @@ def main():
     e2e = None
     cpu = None
     if not args.no_e2e:
+        import psutil
+
+        # pinned host buffers for every rank on this node must fit comfortably in RAM
+        local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+        pipelined = 2 * (16 << m) * local_world <= 0.45 * psutil.virtual_memory().total
         h_in = torch.empty(lay.local_len, dtype=torch.complex128, pin_memory=True)
-        h_out = torch.empty(lay.local_len, dtype=torch.complex128, pin_memory=True)
+        h_out = torch.empty(lay.local_len, dtype=torch.complex128, pin_memory=True) if pipelined else h_in
         state.store_host(h_in)
         barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        # every step: pinned H2D of its input, the circuit, D2H of its result; the
-        # public run_pipelined overlaps step i+1's upload / step i-1's download with step i
-        sv.run_pipelined(lay, timed, [h_in] * len(timed), [h_out] * len(timed), fabric, fusion=fcfg)
+        # every step: pinned H2D of its input, the circuit, D2H of its result
+        if pipelined:  # public run_pipelined overlaps step i+1's upload / step i-1's download with step i
+            sv.run_pipelined(lay, timed, [h_in] * len(timed), [h_out] * len(timed), fabric, fusion=fcfg)
+        else:  # one host buffer per rank: sequential upload -> gates -> download
+            for c in timed:
+                state.load_host(h_in)
+                sv.run_circuit(state, c, fabric, fusion=fcfg)
+                state.store_host(h_in)
         e1.record(stream)
         torch.cuda.synchronize()
         e2e_ms = e0.elapsed_time(e1)
@@ -407,8 +417,9 @@ def main():
         e2e = {"value": round(eff / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
                "h2d_bytes_per_step": (16 << m) * world, "d2h_bytes_per_step": (16 << m) * world,
                "ms_per_step": round(e2e_ms / len(timed), 3),
-               "path": "run_pipelined: LocalState.load_host (sv_copy, H2D stream) -> run_circuit -> "
-                       "LocalState.store_host (sv_copy, D2H stream), two device slots"}
+               "path": ("run_pipelined: LocalState.load_host (sv_copy, H2D stream) -> run_circuit -> "
+                        "LocalState.store_host (sv_copy, D2H stream), two device slots") if pipelined else
+                       "sequential LocalState.load_host -> run_circuit -> store_host (host RAM bound)"}
         if rank == 0 and world == 1 and not args.no_cpu_baseline:
             cpu = cpu_baseline(sv, h_in, n, timed[0], args.cpu_seconds)
         del h_in, h_out
