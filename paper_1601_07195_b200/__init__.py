@@ -60,7 +60,7 @@ from .distributed import (
     make_exchange_plan,
     plan_gate,
 )
-from .engine import GateRecord, run_circuit, run_pipelined
+from .engine import CircuitGraph, GateRecord, run_circuit, run_pipelined
 from .passes import Pass, execute_pass, plan_passes
 from .errors import CircuitParseError, FusionContractError, LayoutError, ResourceError, TransportError
 from .fusion import (

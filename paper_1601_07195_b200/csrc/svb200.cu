@@ -93,6 +93,7 @@ __device__ __forceinline__ double2 shfl_xor2(double2 v, int mask) {
 
 constexpr int BLK = 256;
 constexpr int UNROLL = 4;
+constexpr int PUNROLL = 8;  // pair mode: 8 pairs (256 B of loads) in flight per thread
 enum { MODE_SINGLE = 0, MODE_CTL = 1, MODE_PRED = 2 };
 
 template <int MODE>
@@ -100,17 +101,17 @@ __device__ __forceinline__ uint64_t vmap(uint64_t v, int c) {
   return MODE == MODE_CTL ? insert_one(v, c) : v;
 }
 
-// Pair mode (tv >= 5): each thread owns UNROLL pairs; a warp's 32 consecutive
+// Pair mode (tv >= 5): each thread owns PUNROLL pairs; a warp's 32 consecutive
 // pairs give two fully coalesced 512-B streams (a[i0], a[i0 + 2^tv]).
 template <int MODE>
 __global__ void __launch_bounds__(BLK) k_pairs(double2 *__restrict__ a, uint64_t npairs, int tv, int c,
                                                GateQ q) {
   const uint64_t tb = 1ull << tv;
-  const uint64_t p0 = (uint64_t)blockIdx.x * (BLK * UNROLL) + threadIdx.x;
-  double2 x0[UNROLL], x1[UNROLL];
-  uint64_t i0[UNROLL], i1[UNROLL];
+  const uint64_t p0 = (uint64_t)blockIdx.x * (BLK * PUNROLL) + threadIdx.x;
+  double2 x0[PUNROLL], x1[PUNROLL];
+  uint64_t i0[PUNROLL], i1[PUNROLL];
 #pragma unroll
-  for (int u = 0; u < UNROLL; ++u) {
+  for (int u = 0; u < PUNROLL; ++u) {
     const uint64_t p = p0 + (uint64_t)u * BLK;
     const uint64_t v0 = insert_zero(p, tv);
     i0[u] = vmap<MODE>(v0, c);
@@ -121,7 +122,7 @@ __global__ void __launch_bounds__(BLK) k_pairs(double2 *__restrict__ a, uint64_t
     }
   }
 #pragma unroll
-  for (int u = 0; u < UNROLL; ++u) {
+  for (int u = 0; u < PUNROLL; ++u) {
     const uint64_t p = p0 + (uint64_t)u * BLK;
     if (p >= npairs) continue;
     double2 n0 = mix(x0[u], x1[u], q.v[0], q.v[1], q.v[2], q.v[3]);
@@ -770,7 +771,7 @@ int launch_local(double2 *a, int vbits, int tv, int c, const GateQ &q, cudaStrea
     k_shfl<MODE><<<grid_for(nvirt, BLK * UNROLL), BLK, 0, st>>>(a, nvirt, tv, c, q);
   } else {
     const uint64_t np = nvirt >> 1;
-    k_pairs<MODE><<<grid_for(np, BLK * UNROLL), BLK, 0, st>>>(a, np, tv, c, q);
+    k_pairs<MODE><<<grid_for(np, BLK * PUNROLL), BLK, 0, st>>>(a, np, tv, c, q);
   }
   return after_launch(what);
 }

@@ -156,3 +156,29 @@ def test_exchange_stage_abi_guards():
     assert L.sv_exchange_stage(a.data_ptr(), b.data_ptr(), 6, 1, g, 1, st) == _lib.SV_EINVAL  # control 7 not local
     assert L.sv_exchange_stage(a.data_ptr(), b.data_ptr(), 6, 1, g, 0, st) == _lib.SV_EINVAL
     assert L.sv_apply_gates(a.data_ptr(), 6, g, 1, 0, st) == _lib.SV_EINVAL  # target 6 not local
+
+
+def test_run_pipelined_matches_run_circuit():
+    n = 16
+    rng = np.random.default_rng(44)
+    circs = [sv.random_circuit(n, 30, rng, controlled_fraction=0.4) for _ in range(3)]
+    ins = [torch.from_numpy(random_state(rng, n)).pin_memory() for _ in range(3)]
+    outs = [torch.empty_like(x).pin_memory() for x in ins]
+    sv.run_pipelined(sv.Layout(n), circs, ins, outs, fusion=sv.FusionConfig(l_c=12, passes=True))
+    torch.cuda.synchronize()
+    for c, x, y in zip(circs, ins, outs):
+        want = run_oracle(x.numpy(), c.gates)
+        assert bits_equal(y.numpy(), want)
+
+
+def test_circuit_graph_replay_bitwise():
+    n = 20
+    rng = np.random.default_rng(45)
+    v = random_state(rng, n)
+    circ = sv.random_circuit(n, 60, rng, controlled_fraction=0.3)
+    st = sv.state_from_global(sv.Layout(n), v, device=DEV)
+    g = sv.CircuitGraph(st, circ, fusion=sv.FusionConfig(l_c=13, passes=True))
+    g.replay()
+    g.replay()
+    want = run_oracle(run_oracle(v, circ.gates), circ.gates)
+    assert bits_equal(st.to_numpy(), want)

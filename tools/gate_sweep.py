@@ -80,6 +80,32 @@ def main():
                                                           for j in range(G - 1)]
                 ms = timeit(lambda: sv.kernels.apply_gates(st.amps, gates), a.reps)
                 emit(kind="stage", k=k, gates=G, ms=round(ms, 4), phys_gbps=round((32 << n) / ms / 1e6, 1))
+    if "exchange" in what:
+        # loopback: both "ranks" on this GPU, so the partner slice is local HBM -- this checks
+        # the exchange kernels' own efficiency (HBM-bound here; NVLink-bound across GPUs)
+        from paper_1601_07195_b200 import _lib
+
+        m = n - 1
+        a = torch.empty(1 << m, dtype=torch.complex128, device="cuda")
+        b = torch.empty(1 << m, dtype=torch.complex128, device="cuda")
+        a.copy_(st.amps[: 1 << m])
+        b.copy_(st.amps[1 << m:])
+        L = _lib.load()
+        s = torch.cuda.current_stream().cuda_stream
+        for c_local in (-1, 0, 3, m - 1):
+            ms = timeit(lambda: (_lib.check(L.sv_exchange(a.data_ptr(), b.data_ptr(), m, 1, c_local, q.qbuf(), s)),
+                                 _lib.check(L.sv_exchange(b.data_ptr(), a.data_ptr(), m, 0, c_local, q.qbuf(), s))),
+                        a.reps)
+            touched = (32 << m) if c_local < 0 else (16 << m)
+            emit(kind="exchange_loopback", c_local=c_local, ms=round(ms, 4),
+                 hbm_gbps=round(2 * touched / ms / 1e6, 1))
+        stage = [sv.GateOp(sv.hadamard(), n - 1)] + [sv.GateOp(sv.phase_r(j + 2), n - 1, j) for j in range(20)]
+        ga = sv.kernels.gate_array(stage)
+        ms = timeit(lambda: (_lib.check(L.sv_exchange_stage(a.data_ptr(), b.data_ptr(), m, 1, ga, len(stage), s)),
+                             _lib.check(L.sv_exchange_stage(b.data_ptr(), a.data_ptr(), m, 0, ga, len(stage), s))),
+                    a.reps)
+        emit(kind="exchange_stage_loopback", gates=len(stage), ms=round(ms, 4), hbm_gbps=round(2 * (32 << m) / ms / 1e6, 1))
+        del a, b
     if "qft" in what:
         circ = sv.build_qft(n)
         for l_c in (None, 12, 13, "p12", "p13"):
@@ -103,6 +129,12 @@ def main():
             ms = timeit(lambda: sv.run_circuit(s20, circ, fusion=fusion), a.reps)
             emit(kind="config1", n=m, l_c=l_c, gates=200, ms=round(ms, 3), us_per_gate=round(ms * 1e3 / 200, 2),
                  eff_gbps=round(200 * (32 << m) / ms / 1e6, 1))
+        for l_c in (None, 13):
+            fusion = None if l_c is None else sv.FusionConfig(l_c=l_c, passes=True)
+            g = sv.CircuitGraph(s20, circ, fusion=fusion)
+            ms = timeit(g.replay, a.reps)
+            emit(kind="config1_graph", n=m, passes=l_c, gates=200, ms=round(ms, 3),
+                 us_per_gate=round(ms * 1e3 / 200, 2), eff_gbps=round(200 * (32 << m) / ms / 1e6, 1))
 
 
 if __name__ == "__main__":
