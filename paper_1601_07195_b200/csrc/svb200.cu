@@ -602,6 +602,15 @@ __global__ void __launch_bounds__(BLK) k_stage_pairs(double2 *__restrict__ a, ui
 // remote traffic with the local read/update/write (the paper's T = max(Tcomp,
 // Tcomm) pipeline, distributed.py:205-290, without staging buffers).
 
+// Make this CTA's remote stores performed at system scope before it retires,
+// so the stream-ordered fence that follows the grid publishes them to the
+// partner: the barrier orders every thread's stores before thread 0's
+// cumulative fence.sc.sys (one fence per CTA instead of one per thread).
+__device__ __forceinline__ void cta_release_system() {
+  __syncthreads();
+  if (threadIdx.x == 0) __threadfence_system();
+}
+
 __global__ void __launch_bounds__(BLK) k_exchange(double2 *__restrict__ mine, double2 *__restrict__ theirs,
                                                   uint64_t count, uint64_t base, int c_local, int own_is_zero,
                                                   GateQ q) {
@@ -632,9 +641,7 @@ __global__ void __launch_bounds__(BLK) k_exchange(double2 *__restrict__ mine, do
     mine[jj[u]] = keep;
     theirs[jj[u]] = ret;
   }
-  // Make the remote stores globally performed before the grid retires, so the
-  // stream-ordered fence that follows publishes them to the partner.
-  __threadfence_system();
+  cta_release_system();
 }
 
 // A whole stage of gates sharing one global target in ONE exchange: every
@@ -666,7 +673,7 @@ __global__ void __launch_bounds__(BLK) k_exchange_stage(double2 *__restrict__ mi
     mine[jj[u]] = own_is_zero ? x0[u] : x1[u];
     theirs[jj[u]] = own_is_zero ? x1[u] : x0[u];
   }
-  __threadfence_system();
+  cta_release_system();
 }
 
 // ------------------------------------------------------------ register helpers

@@ -86,26 +86,27 @@ def main():
         from paper_1601_07195_b200 import _lib
 
         m = n - 1
-        a = torch.empty(1 << m, dtype=torch.complex128, device="cuda")
-        b = torch.empty(1 << m, dtype=torch.complex128, device="cuda")
-        a.copy_(st.amps[: 1 << m])
-        b.copy_(st.amps[1 << m:])
+        ta = torch.empty(1 << m, dtype=torch.complex128, device="cuda")
+        tb = torch.empty(1 << m, dtype=torch.complex128, device="cuda")
+        ta.copy_(st.amps[: 1 << m])
+        tb.copy_(st.amps[1 << m:])
         L = _lib.load()
         s = torch.cuda.current_stream().cuda_stream
         for c_local in (-1, 0, 3, m - 1):
-            ms = timeit(lambda: (_lib.check(L.sv_exchange(a.data_ptr(), b.data_ptr(), m, 1, c_local, q.qbuf(), s)),
-                                 _lib.check(L.sv_exchange(b.data_ptr(), a.data_ptr(), m, 0, c_local, q.qbuf(), s))),
+            ms = timeit(lambda: (_lib.check(L.sv_exchange(ta.data_ptr(), tb.data_ptr(), m, 1, c_local, q.qbuf(), s)),
+                                 _lib.check(L.sv_exchange(tb.data_ptr(), ta.data_ptr(), m, 0, c_local, q.qbuf(), s))),
                         a.reps)
             touched = (32 << m) if c_local < 0 else (16 << m)
             emit(kind="exchange_loopback", c_local=c_local, ms=round(ms, 4),
                  hbm_gbps=round(2 * touched / ms / 1e6, 1))
         stage = [sv.GateOp(sv.hadamard(), n - 1)] + [sv.GateOp(sv.phase_r(j + 2), n - 1, j) for j in range(20)]
         ga = sv.kernels.gate_array(stage)
-        ms = timeit(lambda: (_lib.check(L.sv_exchange_stage(a.data_ptr(), b.data_ptr(), m, 1, ga, len(stage), s)),
-                             _lib.check(L.sv_exchange_stage(b.data_ptr(), a.data_ptr(), m, 0, ga, len(stage), s))),
+        ms = timeit(lambda: (_lib.check(L.sv_exchange_stage(ta.data_ptr(), tb.data_ptr(), m, 1, ga, len(stage), s)),
+                             _lib.check(L.sv_exchange_stage(tb.data_ptr(), ta.data_ptr(), m, 0, ga, len(stage), s))),
                     a.reps)
-        emit(kind="exchange_stage_loopback", gates=len(stage), ms=round(ms, 4), hbm_gbps=round(2 * (32 << m) / ms / 1e6, 1))
-        del a, b
+        emit(kind="exchange_stage_loopback", gates=len(stage), ms=round(ms, 4),
+             hbm_gbps=round(2 * (32 << m) / ms / 1e6, 1))
+        del ta, tb
     if "qft" in what:
         circ = sv.build_qft(n)
         for l_c in (None, 12, 13, "p12", "p13"):
