@@ -490,7 +490,10 @@ struct StageParams {
   StageGate g[STAGE_MAX_GATES];
 };
 
-constexpr int SUNROLL = 4;
+#ifndef SV_SUNROLL
+#define SV_SUNROLL 2  // measured best of 1/2/4/8 on B200 (more resident warps hide the per-gate chains)
+#endif
+constexpr int SUNROLL = SV_SUNROLL;
 
 // One gate of a stage on U register pairs.  ok0[u] caches nonzero2(x0[u]):
 // a phase gate leaves x0 untouched on its fast path, so a stage of phases
@@ -542,12 +545,78 @@ __device__ __forceinline__ void stage_gate_any(int kind, double2 (&x0)[SUNROLL],
     stage_gate<KIND_GENERAL, SUNROLL>(x0, x1, ok0, idx, cm, q);
 }
 
-// SIG 0: any mix of kinds.  SIG 1: gate 0 of any kind, every later gate a phase
-// (a transform stage H(k), R(k, c)...): the gate loop then has no kind branch,
-// so no register shuffling between branch variants.
+// Speculative fast path: general gates run the full mix(); diagonal and phase
+// gates update in place with their products only and raise `suspect` on any
+// zero component (the one case where the skipped signed-zero term of mix() can
+// change a bit).  The kernels store nothing until the stage is done, so a
+// suspect thread reloads its pairs from memory and replays the stage through
+// stage_apply_exact.  No per-gate branch and no register copies on the common
+// path.
+template <int KIND>
+__device__ __forceinline__ void stage_gate_fast(double2 (&x0)[SUNROLL], double2 (&x1)[SUNROLL],
+                                                bool (&ok0)[SUNROLL], const uint64_t (&idx)[SUNROLL],
+                                                uint64_t cm, const double *qp, bool &suspect) {
+  double q[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) q[i] = qp[i];
+#pragma unroll
+  for (int u = 0; u < SUNROLL; ++u) {
+    if (cm && !(idx[u] & cm)) continue;
+    if (KIND == KIND_GENERAL) {
+      pair_update<KIND_GENERAL>(x0[u], x1[u], q);
+      ok0[u] = nonzero2(x0[u]);
+    } else if (KIND == KIND_PHASE) {
+      x1[u] = cmul(q[6], q[7], x1[u]);
+      suspect |= !(ok0[u] & nonzero2(x1[u]));
+    } else {
+      x0[u] = cmul(q[0], q[1], x0[u]);
+      x1[u] = cmul(q[6], q[7], x1[u]);
+      ok0[u] = nonzero2(x0[u]);
+      suspect |= !(ok0[u] & nonzero2(x1[u]));
+    }
+  }
+}
+
 template <int SIG>
-__device__ __forceinline__ void stage_apply(double2 (&x0)[SUNROLL], double2 (&x1)[SUNROLL],
-                                            const uint64_t (&idx)[SUNROLL], const StageParams &P) {
+__device__ __forceinline__ bool stage_apply_fast(double2 (&x0)[SUNROLL], double2 (&x1)[SUNROLL],
+                                                 const uint64_t (&idx)[SUNROLL], const StageParams &P) {
+  bool ok0[SUNROLL], suspect = false;
+#pragma unroll
+  for (int u = 0; u < SUNROLL; ++u) ok0[u] = nonzero2(x0[u]);
+  int gi = 0;
+  if (SIG == 1) {
+    const StageGate &G = P.g[0];
+    const uint64_t cm = G.control >= 0 ? (1ull << G.control) : 0ull;
+    if (G.kind == KIND_GENERAL)
+      stage_gate_fast<KIND_GENERAL>(x0, x1, ok0, idx, cm, G.q, suspect);
+    else if (G.kind == KIND_DIAG)
+      stage_gate_fast<KIND_DIAG>(x0, x1, ok0, idx, cm, G.q, suspect);
+    else
+      stage_gate_fast<KIND_PHASE>(x0, x1, ok0, idx, cm, G.q, suspect);
+    for (gi = 1; gi < P.ngates; ++gi) {
+      const StageGate &H = P.g[gi];
+      stage_gate_fast<KIND_PHASE>(x0, x1, ok0, idx, H.control >= 0 ? (1ull << H.control) : 0ull, H.q, suspect);
+    }
+    return suspect;
+  }
+  for (; gi < P.ngates; ++gi) {
+    const StageGate &G = P.g[gi];
+    const uint64_t cm = G.control >= 0 ? (1ull << G.control) : 0ull;
+    if (G.kind == KIND_PHASE)
+      stage_gate_fast<KIND_PHASE>(x0, x1, ok0, idx, cm, G.q, suspect);
+    else if (G.kind == KIND_DIAG)
+      stage_gate_fast<KIND_DIAG>(x0, x1, ok0, idx, cm, G.q, suspect);
+    else
+      stage_gate_fast<KIND_GENERAL>(x0, x1, ok0, idx, cm, G.q, suspect);
+  }
+  return suspect;
+}
+
+// The exact path (replay): per-gate zero tests, falls back to mix() per pair.
+// SIG 0: any mix of kinds.  SIG 1: gate 0 of any kind, every later gate a phase.
+template <int SIG>
+__device__ __forceinline__ void stage_apply_exact(double2 (&x0)[SUNROLL], double2 (&x1)[SUNROLL],
+                                               const uint64_t (&idx)[SUNROLL], const StageParams &P) {
   bool ok0[SUNROLL];
 #pragma unroll
   for (int u = 0; u < SUNROLL; ++u) ok0[u] = nonzero2(x0[u]);
@@ -583,7 +652,16 @@ __global__ void __launch_bounds__(BLK) k_stage_pairs(double2 *__restrict__ a, ui
       x1[u] = a[i0[u] | tb];
     }
   }
-  stage_apply<SIG>(x0, x1, i0, P);
+  if (__builtin_expect(stage_apply_fast<SIG>(x0, x1, i0, P), 0)) {
+#pragma unroll
+    for (int u = 0; u < SUNROLL; ++u) {
+      if (p0 + (uint64_t)u * BLK < npairs) {
+        x0[u] = a[i0[u]];
+        x1[u] = a[i0[u] | tb];
+      }
+    }
+    stage_apply_exact<SIG>(x0, x1, i0, P);
+  }
 #pragma unroll
   for (int u = 0; u < SUNROLL; ++u) {
     const uint64_t p = p0 + (uint64_t)u * BLK;
@@ -652,11 +730,11 @@ template <int SIG>
 __global__ void __launch_bounds__(BLK) k_exchange_stage(double2 *__restrict__ mine, double2 *__restrict__ theirs,
                                                         uint64_t count, uint64_t base, int own_is_zero,
                                                         const StageParams P) {
-  const uint64_t p0 = (uint64_t)blockIdx.x * (BLK * UNROLL) + threadIdx.x;
-  double2 x0[UNROLL], x1[UNROLL];
-  uint64_t jj[UNROLL];
+  const uint64_t p0 = (uint64_t)blockIdx.x * (BLK * SUNROLL) + threadIdx.x;
+  double2 x0[SUNROLL], x1[SUNROLL];
+  uint64_t jj[SUNROLL];
 #pragma unroll
-  for (int u = 0; u < UNROLL; ++u) {
+  for (int u = 0; u < SUNROLL; ++u) {
     const uint64_t p = p0 + (uint64_t)u * BLK;
     jj[u] = base + p;
     if (p < count) {
@@ -665,9 +743,19 @@ __global__ void __launch_bounds__(BLK) k_exchange_stage(double2 *__restrict__ mi
       x1[u] = own_is_zero ? at : am;
     }
   }
-  stage_apply<SIG>(x0, x1, jj, P);
+  if (__builtin_expect(stage_apply_fast<SIG>(x0, x1, jj, P), 0)) {
 #pragma unroll
-  for (int u = 0; u < UNROLL; ++u) {
+    for (int u = 0; u < SUNROLL; ++u) {
+      if (p0 + (uint64_t)u * BLK < count) {
+        const double2 am = mine[jj[u]], at = theirs[jj[u]];
+        x0[u] = own_is_zero ? am : at;
+        x1[u] = own_is_zero ? at : am;
+      }
+    }
+    stage_apply_exact<SIG>(x0, x1, jj, P);
+  }
+#pragma unroll
+  for (int u = 0; u < SUNROLL; ++u) {
     const uint64_t p = p0 + (uint64_t)u * BLK;
     if (p >= count) continue;
     mine[jj[u]] = own_is_zero ? x0[u] : x1[u];
