@@ -340,12 +340,26 @@ __device__ __forceinline__ int reg_off(int j, const int m0, const int m1, const 
 // branch (see stage_gate).  FULL: every pair active (pm == 0xFFFF).
 constexpr int TG = 2;
 
-template <int TB, int KIND, bool FULL>
-__device__ __forceinline__ void tile_gate_k(double2 (&r)[TRN], uint32_t pm, const double *qp) {
+// SPEC (speculative) variant: diagonal/phase gates update in place with their
+// products only and raise `suspect` on any zero component; the kernel then
+// replays the whole tile from global memory with the exact variant (k_tile).
+template <int TB, int KIND, bool FULL, bool SPEC>
+__device__ __forceinline__ void tile_gate_k(double2 (&r)[TRN], uint32_t pm, const double *qp, bool &suspect) {
   double q[8];  // once per gate in registers, not one constant-bank load per pair
 #pragma unroll
   for (int i = 0; i < 8; ++i) q[i] = qp[i];
 #define PAIRS(k) ((((k) >> TB) << (TB + 1)) | ((k) & ((1 << TB) - 1)))  // k-th j with bit TB clear
+  if (SPEC && KIND != KIND_GENERAL) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int j = PAIRS(k);
+      if (!(FULL || ((pm >> j) & 1u))) continue;
+      if (KIND == KIND_DIAG) r[j] = cmul(q[0], q[1], r[j]);
+      r[j | (1 << TB)] = cmul(q[6], q[7], r[j | (1 << TB)]);
+      suspect |= !(nonzero2(r[j]) & nonzero2(r[j | (1 << TB)]));
+    }
+    return;
+  }
 #pragma unroll
   for (int grp = 0; grp < 8 / TG; ++grp) {
     if (KIND == KIND_GENERAL) {
@@ -385,40 +399,32 @@ __device__ __forceinline__ void tile_gate_k(double2 (&r)[TRN], uint32_t pm, cons
   }
 }
 
-template <int TB, int KIND>
-__device__ __forceinline__ void tile_gate_all(double2 (&r)[TRN], const double *qp) {
-  tile_gate_k<TB, KIND, true>(r, 0xFFFFu, qp);
-}
-
-template <int TB>
-__device__ __forceinline__ void tile_gate(double2 (&r)[TRN], uint32_t pm, int kind, const double *q) {
+template <int TB, bool SPEC>
+__device__ __forceinline__ void tile_gate(double2 (&r)[TRN], uint32_t pm, int kind, const double *q, bool &sus) {
   if (pm == 0u) return;
   if (pm == 0xFFFFu) {  // uncontrolled, or control decided per thread/CTA: straight-line code
     if (kind == KIND_GENERAL)
-      tile_gate_all<TB, KIND_GENERAL>(r, q);
+      tile_gate_k<TB, KIND_GENERAL, true, SPEC>(r, pm, q, sus);
     else if (kind == KIND_PHASE)
-      tile_gate_all<TB, KIND_PHASE>(r, q);
+      tile_gate_k<TB, KIND_PHASE, true, SPEC>(r, pm, q, sus);
     else
-      tile_gate_all<TB, KIND_DIAG>(r, q);
+      tile_gate_k<TB, KIND_DIAG, true, SPEC>(r, pm, q, sus);
     return;
   }
   if (kind == KIND_GENERAL)
-    tile_gate_k<TB, KIND_GENERAL, false>(r, pm, q);
+    tile_gate_k<TB, KIND_GENERAL, false, SPEC>(r, pm, q, sus);
   else if (kind == KIND_PHASE)
-    tile_gate_k<TB, KIND_PHASE, false>(r, pm, q);
+    tile_gate_k<TB, KIND_PHASE, false, SPEC>(r, pm, q, sus);
   else
-    tile_gate_k<TB, KIND_DIAG, false>(r, pm, q);
+    tile_gate_k<TB, KIND_DIAG, false, SPEC>(r, pm, q, sus);
 }
 
-template <int T>
-__global__ void __launch_bounds__(1 << (T - TR), (T <= 12) ? 2 : 1)
-    k_tile(double2 *__restrict__ a, const TileParams P) {
+// One tile through the run: load (natural layout), segments with transposes,
+// back to the natural layout in registers (the caller stores).
+template <int T, bool SPEC>
+__device__ __forceinline__ void tile_body(const double2 *__restrict__ g, uint64_t tile0, int tid,
+                                          const TileParams &P, double2 *s, double2 (&r)[TRN], bool &suspect) {
   constexpr int NT = 1 << (T - TR);
-  extern __shared__ double2 s[];
-  const uint64_t tile0 = (uint64_t)blockIdx.x << T;
-  double2 *__restrict__ g = a + tile0;
-  const int tid = threadIdx.x;
-  double2 r[TRN];
 #pragma unroll
   for (int j = 0; j < TRN; ++j) r[j] = g[tid + j * NT];
   // current layout: natural (register bits = top four tile bits, thread bits ascending)
@@ -451,10 +457,10 @@ __global__ void __launch_bounds__(1 << (T - TR), (T <= 12) ? 2 : 1)
       else if (G.cmode == 3)
         pm = ((tile0 >> G.cabove) & 1ull) ? 0xFFFFu : 0u;
       switch (G.tb) {
-        case 0: tile_gate<0>(r, pm, G.kind, G.q); break;
-        case 1: tile_gate<1>(r, pm, G.kind, G.q); break;
-        case 2: tile_gate<2>(r, pm, G.kind, G.q); break;
-        default: tile_gate<3>(r, pm, G.kind, G.q); break;
+        case 0: tile_gate<0, SPEC>(r, pm, G.kind, G.q, suspect); break;
+        case 1: tile_gate<1, SPEC>(r, pm, G.kind, G.q, suspect); break;
+        case 2: tile_gate<2, SPEC>(r, pm, G.kind, G.q, suspect); break;
+        default: tile_gate<3, SPEC>(r, pm, G.kind, G.q, suspect); break;
       }
     }
   }
@@ -466,6 +472,23 @@ __global__ void __launch_bounds__(1 << (T - TR), (T <= 12) ? 2 : 1)
 #pragma unroll
     for (int j = 0; j < TRN; ++j) r[j] = s[swz(tid + j * NT)];
   }
+}
+
+// SPEC = true when the run holds diagonal/phase gates (host-chosen): speculative
+// in-place updates, and on any zero component the whole tile is replayed
+// exactly from global memory (nothing stored yet).  SPEC = false: exact path.
+template <int T, bool SPEC>
+__global__ void __launch_bounds__(1 << (T - TR), (T <= 12) ? 2 : 1)
+    k_tile(double2 *__restrict__ a, const TileParams P) {
+  constexpr int NT = 1 << (T - TR);
+  extern __shared__ double2 s[];
+  const uint64_t tile0 = (uint64_t)blockIdx.x << T;
+  double2 *__restrict__ g = a + tile0;
+  const int tid = threadIdx.x;
+  double2 r[TRN];
+  bool suspect = false;
+  tile_body<T, SPEC>(g, tile0, tid, P, s, r, suspect);
+  if (SPEC && __syncthreads_or(suspect)) tile_body<T, false>(g, tile0, tid, P, s, r, suspect);
 #pragma unroll
   for (int j = 0; j < TRN; ++j) g[tid + j * NT] = r[j];
 }
@@ -982,15 +1005,24 @@ int plan_tile(const sv_gate *gates, int n, int T, TileParams &P) {
   return gi;
 }
 
-template <int T>
-int launch_tile_t(double2 *a, int m, const TileParams &P, cudaStream_t st) {
+template <int T, bool SPEC>
+int launch_tile_ts(double2 *a, int m, const TileParams &P, cudaStream_t st) {
   const size_t smem = sizeof(double2) << T;
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k_tile<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(k_tile<T, SPEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return fail(SV_ECUDA, "tile: smem attribute: %s", cudaGetErrorString(e));
   }
-  k_tile<T><<<(unsigned)(1ull << (m - T)), 1 << (T - TR), smem, st>>>(a, P);
+  k_tile<T, SPEC><<<(unsigned)(1ull << (m - T)), 1 << (T - TR), smem, st>>>(a, P);
   return after_launch("k_tile");
+}
+
+template <int T>
+int launch_tile_t(double2 *a, int m, const TileParams &P, cudaStream_t st) {
+  int ndiag = 0, ngates = 0;
+  for (int s = 0; s < P.nsegs; ++s) ngates = P.seg[s].first + P.seg[s].count;
+  for (int i = 0; i < ngates; ++i) ndiag += P.g[i].kind != KIND_GENERAL;
+  // speculation pays when diagonal/phase updates dominate the run (transform tails)
+  return 2 * ndiag >= ngates ? launch_tile_ts<T, true>(a, m, P, st) : launch_tile_ts<T, false>(a, m, P, st);
 }
 
 int launch_tile(double2 *a, int m, int T, const TileParams &P, cudaStream_t st) {

@@ -182,3 +182,24 @@ def test_circuit_graph_replay_bitwise():
     g.replay()
     want = run_oracle(run_oracle(v, circ.gates), circ.gates)
     assert bits_equal(st.to_numpy(), want)
+
+
+@pytest.mark.parametrize("n", [13, 17])
+def test_speculative_paths_replay_exactly_on_zeros(n):
+    """Diagonal/phase-dominated runs take the speculative kernels; states salted with +-0 and
+    'nice' values force the exact replay -- bits must still equal the oracle."""
+    rng = np.random.default_rng(900 + n)
+    diag = [sv.phase_r(2), sv.phase_r(5).dagger(), sv.pauli_z(), sv.rotation_z(0.7),
+            sv.GateMatrix([[1j, 0], [0, -1]]), sv.GateMatrix.unchecked([[1, -0.0], [0.0, 1j]])]
+    for trial in range(4):
+        v = with_zeros(rng, n, frac=0.3) if trial % 2 else np.full(1 << n, 2.0 ** (-n / 2), dtype=np.complex128)
+        ops = []
+        for _ in range(80):
+            t = int(rng.integers(n if trial < 2 else 12))
+            c = None if rng.random() < 0.3 else int((t + 1 + rng.integers(n - 1)) % n)
+            ops.append(sv.GateOp(diag[int(rng.integers(len(diag)))], t, c))
+        ops.insert(0, sv.GateOp(sv.hadamard(), n - 1))
+        a = torch.from_numpy(v.copy()).to(DEV)
+        sv.kernels.apply_gates(a, ops)
+        torch.cuda.synchronize()
+        assert bits_equal(a.cpu().numpy(), run_oracle(v, ops)), trial
