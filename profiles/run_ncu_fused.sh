@@ -1,8 +1,9 @@
 #!/bin/bash
-# ncu captures of the fused kernels (stage pass, register tile) -- one GPU.
+# ncu captures of the fused kernels (stage pass, register tile) and the QFT pass-plan launch list -- one GPU.
 set -e
 OUT=${OUT:-gpurun_out}
 CMD="python tools/profile_kernels.py 28"
 $CMD > $OUT/ncu_fused_plain.log 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_fused.csv $CMD > $OUT/ncu_fl.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_stage_pairs -s 1 -c 1 -o $OUT/prof_stage $CMD > $OUT/ncu_stage.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_tile -s 2 -c 2 -o $OUT/prof_tile $CMD > $OUT/ncu_tile.log 2>&1

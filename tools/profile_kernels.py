@@ -1,4 +1,9 @@
-"""Small driver for ncu captures of the fused kernels (run under gpurun; see profiles/run_ncu_fused.sh)."""
+"""Small driver for ncu captures of the fused kernels (run under gpurun; see profiles/run_ncu_fused.sh).
+
+Launch order (for ncu -k/-s/-c):  per round, one 30-gate transform stage (k_stage_pairs<1>), one
+64-gate random run on targets < 12 (k_tile<12, false>), then the QFT(n) pass plan (18-ish
+k_stage_pairs<1> stages + one k_tile<12, true> tail).  Two rounds.
+"""
 import sys
 from pathlib import Path
 
@@ -16,10 +21,10 @@ k = n - 2
 ctl = [c for c in range(n) if c != k][:29]
 stage = [sv.GateOp(sv.hadamard(), k)] + [sv.GateOp(sv.phase_r(j + 2), k, c) for j, c in enumerate(ctl)]
 tile = [sv.GateOp(sv.random_unitary(rng), int(rng.integers(12))) for _ in range(64)]
-qft_tail = [op for op in sv.build_qft(n).gates if op.target < 12]
+qft = sv.build_qft(n)
 for _ in range(2):
     sv.kernels.apply_gates(st.amps, stage)
     sv.kernels.apply_gates(st.amps, tile, tile=12)
-    sv.kernels.apply_gates(st.amps, qft_tail, tile=12)
+    sv.run_circuit(st, qft, fusion=sv.FusionConfig(l_c=12, passes=True))
 torch.cuda.synchronize()
 print("ok")
