@@ -375,6 +375,19 @@ def main():
         for k in range(m):
             ks = [unit_ms[j][k] for j in range(len(timed))]
             per_target[k] = round((32 << m) / (float(np.median(ks)) * 1e-3) / 1e9, 1)
+    buckets = {}
+    if args.workload == "controlled" and fusion == "none":
+        # GB/s (16*2^m accounting) by c<t / c>t and by min(c,t)
+        for c_circ, ms in zip(timed, unit_ms):
+            for op, t_ms in zip(c_circ, ms):
+                if op.control is None or op.max_qubit() >= m:
+                    continue
+                lo = min(op.control, op.target)
+                band = "0" if lo == 0 else "1" if lo == 1 else "2-4" if lo <= 4 else ">=5"
+                for key in (f"c<t" if op.control < op.target else "c>t", f"min(c,t)={band}"):
+                    buckets.setdefault(key, []).append(t_ms)
+        buckets = {k: {"gbps": round((16 << m) / (float(np.median(v)) * 1e-3) / 1e9, 1), "gates": len(v)}
+                   for k, v in sorted(buckets.items())}
     nvlink = None
     glob = [r for k, rs in by_kind.items() if k in ("exchange", "pass-global_stage", "pass-global_gate") for r in rs]
     if world > 1 and glob:
@@ -439,6 +452,8 @@ def main():
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks.summary(),
         }
+        if buckets:
+            line["controlled_buckets"] = buckets
         if per_target:
             line["per_target_gbps"] = per_target
         if nvlink:
