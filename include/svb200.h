@@ -85,6 +85,20 @@ int sv_apply_fused(void *amps, int m, int l, const sv_gate *gates, int ngates, v
  * 9 <= tile <= min(m, SV_FUSED_MAX_TILE). */
 int sv_apply_gates(void *amps, int m, const sv_gate *gates, int ngates, int tile, void *stream);
 
+/* Launch-group kinds of the pass planner. */
+#define SV_GROUP_GATES 0 /* one launch per gate (sv_apply_single / sv_apply_controlled) */
+#define SV_GROUP_TILE 1  /* register-tiled run: targets < tile-4 plus up to four higher bits */
+#define SV_GROUP_STAGE 2 /* same-target stage */
+
+/* The planner of sv_apply_gates, exposed (pure host code, no GPU needed):
+ * writes the end index and kind of each launch group, returns the number of
+ * groups (or a negative error).  sv_apply_gates == sv_apply_group over these. */
+int sv_plan_gates(int m, const sv_gate *gates, int ngates, int tile, int32_t *group_end, int32_t *group_kind,
+                  int max_groups);
+
+/* Execute one planned group (kind SV_GROUP_*), e.g. to time groups one by one. */
+int sv_apply_group(void *amps, int m, int kind, const sv_gate *gates, int ngates, int tile, void *stream);
+
 /* A stage of gates that all target the same global qubit, applied in ONE
  * exchange (sv_exchange generalised to a gate list): each pair crosses NVLink
  * once each way.  Controls must be local (< m) or -1; the caller drops gates

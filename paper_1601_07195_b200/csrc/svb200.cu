@@ -317,12 +317,33 @@ struct TileSeg {
   int8_t natural, pad[3];
 };
 
+// A tile is 2^T amplitudes: tile bits 0..T-5 are slice bits 0..T-5 (contiguous
+// runs, coalesced), tile bits T-4..T-1 are the slice bits hb[0..3] (ascending,
+// any positions >= T-4).  hb = {T-4, .., T-1} is the contiguous block of the
+// reference's apply_block; other choices put high qubits into the tile so runs
+// of gates on arbitrary targets fuse (the tile then is a strided gather).
 struct TileParams {
   int nsegs;
   int last_natural;
+  int hb[TR];
   TileSeg seg[TILE_MAX_SEGS];
   TileGate g[TILE_MAX_GATES];
 };
+
+template <int T>
+__device__ __forceinline__ uint64_t tile_base(uint64_t b, const int (&hb)[TR]) {
+  uint64_t x = b << (T - TR);
+#pragma unroll
+  for (int k = 0; k < TR; ++k) x = insert_zero(x, hb[k]);
+  return x;
+}
+
+// slice offset (relative to the tile base) of natural-layout register j of thread tid
+template <int T>
+__device__ __forceinline__ uint64_t tile_off(int tid, int j, const int (&hb)[TR]) {
+  return (uint64_t)tid | ((uint64_t)(j & 1) << hb[0]) | ((uint64_t)((j >> 1) & 1) << hb[1]) |
+         ((uint64_t)((j >> 2) & 1) << hb[2]) | ((uint64_t)((j >> 3) & 1) << hb[3]);
+}
 
 __device__ __forceinline__ int swz(int i) {
   int h = i >> 3;
@@ -422,11 +443,12 @@ __device__ __forceinline__ void tile_gate(double2 (&r)[TRN], uint32_t pm, int ki
 // One tile through the run: load (natural layout), segments with transposes,
 // back to the natural layout in registers (the caller stores).
 template <int T, bool SPEC>
-__device__ __forceinline__ void tile_body(const double2 *__restrict__ g, uint64_t tile0, int tid,
-                                          const TileParams &P, double2 *s, double2 (&r)[TRN], bool &suspect) {
+__device__ __forceinline__ void tile_body(const double2 *__restrict__ a, uint64_t tile0, const int (&hb)[TR],
+                                          int tid, const TileParams &P, double2 *s, double2 (&r)[TRN],
+                                          bool &suspect) {
   constexpr int NT = 1 << (T - TR);
 #pragma unroll
-  for (int j = 0; j < TRN; ++j) r[j] = g[tid + j * NT];
+  for (int j = 0; j < TRN; ++j) r[j] = a[tile0 + tile_off<T>(tid, j, hb)];
   // current layout: natural (register bits = top four tile bits, thread bits ascending)
   int cbase = tid, c0 = NT, c1 = NT << 1, c2 = NT << 2, c3 = NT << 3;
   bool touched = false;
@@ -482,15 +504,18 @@ __global__ void __launch_bounds__(1 << (T - TR), (T <= 12) ? 2 : 1)
     k_tile(double2 *__restrict__ a, const TileParams P) {
   constexpr int NT = 1 << (T - TR);
   extern __shared__ double2 s[];
-  const uint64_t tile0 = (uint64_t)blockIdx.x << T;
-  double2 *__restrict__ g = a + tile0;
+  int hb[TR];
+#pragma unroll
+  for (int k = 0; k < TR; ++k) hb[k] = P.hb[k];
+  const uint64_t tile0 = tile_base<T>(blockIdx.x, hb);  // every non-tile slice bit of this CTA
   const int tid = threadIdx.x;
   double2 r[TRN];
   bool suspect = false;
-  tile_body<T, SPEC>(g, tile0, tid, P, s, r, suspect);
-  if (SPEC && __syncthreads_or(suspect)) tile_body<T, false>(g, tile0, tid, P, s, r, suspect);
+  tile_body<T, SPEC>(a, tile0, hb, tid, P, s, r, suspect);
+  if (SPEC && __syncthreads_or(suspect)) tile_body<T, false>(a, tile0, hb, tid, P, s, r, suspect);
 #pragma unroll
-  for (int j = 0; j < TRN; ++j) g[tid + j * NT] = r[j];
+  for (int j = 0; j < TRN; ++j) a[tile0 + tile_off<T>(tid, j, hb)] = r[j];
+  (void)NT;
 }
 
 // ------------------------------------------------------------ same-target stages
@@ -935,8 +960,15 @@ int classify_kind(const double *q) {
 // Greedy: the register set is the next four distinct targets (padded with the
 // natural bits T-1, T-2, ...); a segment extends while targets stay in it.
 // Returns the number of gates planned (limited by the parameter arrays).
-int plan_tile(const sv_gate *gates, int n, int T, TileParams &P) {
+int plan_tile(const sv_gate *gates, int n, int T, const int (&hb)[TR], TileParams &P) {
   P.nsegs = 0;
+  for (int k = 0; k < TR; ++k) P.hb[k] = hb[k];
+  auto tbit = [&](int g) {  // slice bit -> tile bit, -1 outside the tile
+    if (g < T - TR) return g;
+    for (int k = 0; k < TR; ++k)
+      if (hb[k] == g) return T - TR + k;
+    return -1;
+  };
   int gi = 0;
   while (gi < n && gi < TILE_MAX_GATES && P.nsegs < TILE_MAX_SEGS) {
     int S[TR], ns = 0;
@@ -946,7 +978,7 @@ int plan_tile(const sv_gate *gates, int n, int T, TileParams &P) {
       return false;
     };
     for (int j = gi; j < n && ns < TR; ++j)
-      if (!in_s(gates[j].target)) S[ns++] = gates[j].target;
+      if (!in_s(tbit(gates[j].target))) S[ns++] = tbit(gates[j].target);
     for (int b = T - 1; b >= 0 && ns < TR; --b)
       if (!in_s(b)) S[ns++] = b;
     std::sort(S, S + TR);
@@ -974,22 +1006,22 @@ int plan_tile(const sv_gate *gates, int n, int T, TileParams &P) {
     for (int b = 0; b < TR; ++b) seg.S[b] = (uint8_t)S[b];
     seg.natural = natural ? 1 : 0;
     seg.first = (int16_t)gi;
-    while (gi < n && gi < TILE_MAX_GATES && in_s(gates[gi].target)) {
+    while (gi < n && gi < TILE_MAX_GATES && in_s(tbit(gates[gi].target))) {
       const sv_gate &src = gates[gi];
       TileGate &G = P.g[gi];
       memset(&G, 0, sizeof(G));
       for (int b = 0; b < TR; ++b)
-        if (S[b] == src.target) G.tb = (int8_t)b;
-      const int c = src.control;
+        if (S[b] == tbit(src.target)) G.tb = (int8_t)b;
+      const int c = src.control, tc = c < 0 ? -1 : tbit(c);
       if (c < 0) {
         G.cmode = 0;
-      } else if (in_s(c)) {
+      } else if (tc >= 0 && in_s(tc)) {
         G.cmode = 1;
         for (int b = 0; b < TR; ++b)
-          if (S[b] == c) G.cbit = (int8_t)b;
-      } else if (c < T) {
+          if (S[b] == tc) G.cbit = (int8_t)b;
+      } else if (tc >= 0) {
         G.cmode = 2;
-        G.cbit = (int8_t)c;
+        G.cbit = (int8_t)tc;
       } else {
         G.cmode = 3;
         G.cabove = c;
@@ -1036,13 +1068,13 @@ int launch_tile(double2 *a, int m, int T, const TileParams &P, cudaStream_t st) 
   }
 }
 
-// Run gates (targets < T, controls anywhere) through k_tile, as many launches as
-// the parameter arrays need.
-int run_tile(double2 *a, int m, int T, const sv_gate *gates, int n, cudaStream_t st) {
+// Run gates (targets in the tile: < T-4 or in hb; controls anywhere) through
+// k_tile, as many launches as the parameter arrays need.
+int run_tile(double2 *a, int m, int T, const int (&hb)[TR], const sv_gate *gates, int n, cudaStream_t st) {
   static thread_local TileParams P;  // ~20 KB: keep it off the stack
   int off = 0;
   while (off < n) {
-    const int used = plan_tile(gates + off, n - off, T, P);
+    const int used = plan_tile(gates + off, n - off, T, hb, P);
     const int rc = launch_tile(a, m, T, P, st);
     if (rc != SV_OK) return rc;
     off += used;
@@ -1079,6 +1111,101 @@ int run_stage(double2 *a, int m, const sv_gate *gates, int n, cudaStream_t st) {
   else
     k_stage_pairs<0><<<grid_for(np, BLK * SUNROLL), BLK, 0, st>>>(a, np, t, P);
   return after_launch("k_stage_pairs");
+}
+
+// Native pass planner: the launch group starting at gates[i], returned as its end.
+// Candidate 1, a register-tiled run: targets below L = T-4, or one of up to four
+// higher slice bits taken in order of appearance (the tile then gathers those
+// bits).  Candidate 2, a same-target stage.  Cost model (B200, ms at 2^30
+// amplitudes, compute overlapping HBM): a pass costs max(5, sum of per-gate
+// costs), per gate tile 1.15 general / 0.45 diagonal, stage 0.6 / 0.37.  The
+// stage is taken when it plus a tile over the rest of the candidate run costs
+// less than the candidate run as one tile.  A lone gate is a single-gate launch.
+// Pure host code (sv_plan_gates exposes it).
+int next_group(int m, const sv_gate *gates, int n, int i, int T, int *kind) {
+  (void)m;
+  const int L = T - TR;
+  auto tile_cost = [&](int k) { return classify_kind(gates[k].q) == KIND_GENERAL ? 1.15 : 0.45; };
+  auto pass = [](double c) { return c > 5.0 ? c : 5.0; };
+  int H[TR], nh = 0, ja = i;
+  double ct = 0.0;
+  if (T >= 9) {
+    for (; ja < n && ja - i < TILE_MAX_GATES; ++ja) {
+      const int tt = gates[ja].target;
+      bool in = tt < L;
+      for (int k = 0; k < nh && !in; ++k) in = H[k] == tt;
+      if (!in) {
+        if (nh == TR) break;
+        H[nh++] = tt;
+      }
+      ct += tile_cost(ja);
+    }
+  }
+  const int t0 = gates[i].target;
+  int jb = i + 1;
+  double cs = classify_kind(gates[i].q) == KIND_GENERAL ? 0.6 : 0.37, ctb = tile_cost(i);
+  while (jb < n && gates[jb].target == t0 && jb - i < STAGE_MAX_GATES) {
+    cs += classify_kind(gates[jb].q) == KIND_GENERAL ? 0.6 : 0.37;
+    ctb += tile_cost(jb);
+    ++jb;
+  }
+  const int A = ja - i, B = jb - i;
+  const bool stage_better = B >= A ? pass(cs) <= pass(ct) : pass(cs) + pass(ct - ctb) < pass(ct);
+  if (A <= 1 && B <= 1) {
+    *kind = SV_GROUP_GATES;
+    return i + 1;
+  }
+  if (t0 >= 5 && B > 1 && stage_better) {
+    *kind = SV_GROUP_STAGE;
+    return jb;
+  }
+  if (A > 1) {
+    *kind = SV_GROUP_TILE;
+    return ja;
+  }
+  *kind = SV_GROUP_GATES;
+  return jb;
+}
+
+int exec_group(double2 *a, int m, int T, int kind, const sv_gate *gates, int n, cudaStream_t st) {
+  if (kind == SV_GROUP_STAGE) {
+    for (int k = 1; k < n; ++k)
+      if (gates[k].target != gates[0].target) return fail(SV_EINVAL, "stage group: targets differ");
+    if (n > STAGE_MAX_GATES) return fail(SV_EINVAL, "stage group: more than %d gates", STAGE_MAX_GATES);
+    if (n == 1 || gates[0].target < 5) {
+      for (int k = 0; k < n; ++k) {
+        const int rc = launch_gate(a, m, gates[k], st);
+        if (rc != SV_OK) return rc;
+      }
+      return SV_OK;
+    }
+    return run_stage(a, m, gates, n, st);
+  }
+  if (kind == SV_GROUP_TILE && T >= 9 && n > 1) {
+    const int L = T - TR;
+    int H[TR], nh = 0;
+    for (int k = 0; k < n; ++k) {
+      const int tt = gates[k].target;
+      bool in = tt < L;
+      for (int q = 0; q < nh && !in; ++q) in = H[q] == tt;
+      if (!in) {
+        if (nh == TR) return fail(SV_EINVAL, "tile group: more than %d targets above bit %d", TR, L - 1);
+        H[nh++] = tt;
+      }
+    }
+    for (int b = L; nh < TR; ++b) {  // pad with the natural block bits
+      bool dup = false;
+      for (int q = 0; q < nh; ++q) dup |= H[q] == b;
+      if (!dup) H[nh++] = b;
+    }
+    std::sort(H, H + TR);
+    return run_tile(a, m, T, H, gates, n, st);
+  }
+  for (int k = 0; k < n; ++k) {
+    const int rc = launch_gate(a, m, gates[k], st);
+    if (rc != SV_OK) return rc;
+  }
+  return SV_OK;
 }
 
 int check_gates(const char *who, int m, const sv_gate *gates, int n, int tmax) {
@@ -1160,7 +1287,10 @@ int sv_apply_fused(void *amps, int m, int l, const sv_gate *gates, int ngates, v
   // Tile: 2^12 amplitudes per CTA where the slice allows (64 KiB: two CTAs per
   // SM overlap one tile's HBM traffic with the other's gates), never below l.
   const int T = l > 12 ? l : (m < 12 ? m : 12);
-  if (T >= 9) return run_tile((double2 *)amps, m, T, gates, ngates, (cudaStream_t)stream);
+  if (T >= 9) {
+    const int hb[TR] = {T - 4, T - 3, T - 2, T - 1};  // contiguous 2^T blocks
+    return run_tile((double2 *)amps, m, T, hb, gates, ngates, (cudaStream_t)stream);
+  }
   static thread_local FusedParams P;  // 18 KB: keep it off the stack
   P.ngates = ngates;
   P.pad = 0;
@@ -1177,26 +1307,46 @@ int sv_apply_gates(void *amps, int m, const sv_gate *gates, int ngates, int tile
   const int tmax = m < SV_FUSED_MAX_TILE ? m : SV_FUSED_MAX_TILE;
   const int T = tile > 0 ? tile : tmax;
   if (tile != 0 && (tile < 9 || tile > tmax)) return fail(SV_EINVAL, "sv_apply_gates: tile %d not in [9, %d]", tile, tmax);
-  double2 *a = (double2 *)amps;
-  cudaStream_t st = (cudaStream_t)stream;
   int i = 0;
   while (i < ngates && rc == SV_OK) {
-    const int t = gates[i].target;
-    int j = i + 1;
-    if (T >= 9 && t < T) {
-      while (j < ngates && gates[j].target < T) ++j;
-      rc = (j - i == 1) ? launch_gate(a, m, gates[i], st) : run_tile(a, m, T, gates + i, j - i, st);
-    } else {
-      while (j < ngates && gates[j].target == t && j - i < STAGE_MAX_GATES) ++j;
-      if (j - i == 1 || t < 5) {
-        for (int k = i; k < j && rc == SV_OK; ++k) rc = launch_gate(a, m, gates[k], st);
-      } else {
-        rc = run_stage(a, m, gates + i, j - i, st);
-      }
-    }
+    int kind;
+    const int j = next_group(m, gates, ngates, i, T, &kind);
+    rc = exec_group((double2 *)amps, m, T, kind, gates + i, j - i, (cudaStream_t)stream);
     i = j;
   }
   return rc;
+}
+
+int sv_plan_gates(int m, const sv_gate *gates, int ngates, int tile, int32_t *group_end, int32_t *group_kind,
+                  int max_groups) {
+  if ((!gates && ngates) || !group_end || !group_kind) return fail(SV_EINVAL, "sv_plan_gates: null pointer");
+  if (m < 1 || m > 62 || ngates < 0) return fail(SV_EINVAL, "sv_plan_gates: m=%d / ngates=%d invalid", m, ngates);
+  int rc = check_gates("sv_plan_gates", m, gates, ngates, m);
+  if (rc != SV_OK) return rc;
+  const int tmax = m < SV_FUSED_MAX_TILE ? m : SV_FUSED_MAX_TILE;
+  if (tile != 0 && (tile < 9 || tile > tmax)) return fail(SV_EINVAL, "sv_plan_gates: tile %d not in [9, %d]", tile, tmax);
+  const int T = tile > 0 ? tile : tmax;
+  int i = 0, ng = 0;
+  while (i < ngates) {
+    if (ng == max_groups) return fail(SV_EINVAL, "sv_plan_gates: more than %d groups", max_groups);
+    int kind;
+    i = next_group(m, gates, ngates, i, T, &kind);
+    group_end[ng] = i;
+    group_kind[ng] = kind;
+    ++ng;
+  }
+  return ng;
+}
+
+int sv_apply_group(void *amps, int m, int kind, const sv_gate *gates, int ngates, int tile, void *stream) {
+  if (bad_ptr(amps) || !gates) return fail(SV_EINVAL, "sv_apply_group: null or misaligned pointer");
+  if (m < 1 || m > 62 || ngates < 1) return fail(SV_EINVAL, "sv_apply_group: m=%d / ngates=%d invalid", m, ngates);
+  int rc = check_gates("sv_apply_group", m, gates, ngates, m);
+  if (rc != SV_OK) return rc;
+  const int tmax = m < SV_FUSED_MAX_TILE ? m : SV_FUSED_MAX_TILE;
+  if (tile != 0 && (tile < 9 || tile > tmax)) return fail(SV_EINVAL, "sv_apply_group: tile %d not in [9, %d]", tile, tmax);
+  if (kind < SV_GROUP_GATES || kind > SV_GROUP_STAGE) return fail(SV_EINVAL, "sv_apply_group: kind %d", kind);
+  return exec_group((double2 *)amps, m, tile > 0 ? tile : tmax, kind, gates, ngates, (cudaStream_t)stream);
 }
 
 int sv_exchange_stage(void *mine, void *theirs, int m, int own_is_zero, const sv_gate *gates, int ngates,

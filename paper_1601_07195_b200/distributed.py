@@ -215,10 +215,17 @@ class CudaExecutor:
             _lib.check(_lib.load().sv_exchange_stage(ptr, theirs, m, int(own_is_zero), gate_array(ops), len(ops),
                                                      stream_handle()))
 
-    def local_gates(self, state: LocalState, ops, tile: int = 0) -> None:
-        from .kernels import apply_gates
+    def local_gates(self, state: LocalState, ops, tile: int = 0, group: int | None = None) -> None:
+        """sv_apply_gates (planner inside), or sv_apply_group for one pre-planned group."""
+        from .kernels import apply_gates, gate_array
 
-        apply_gates(state.amps, ops, tile)
+        if group is None:
+            apply_gates(state.amps, ops, tile)
+            return
+        ptr, m = device_view(state.amps)
+        with torch.cuda.device(state.amps.device):
+            _lib.check(_lib.load().sv_apply_group(ptr, m, int(group), gate_array(ops), len(ops), int(tile),
+                                                  stream_handle()))
 
     def synchronize(self, state: LocalState) -> None:
         torch.cuda.current_stream(state.amps.device).synchronize()

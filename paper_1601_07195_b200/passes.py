@@ -57,7 +57,6 @@ def plan_passes(gates, m: int, tile: int = 0) -> list[Pass]:
     grouping ``sv_apply_gates`` applies natively, exposed so each pass can be
     timed and recorded on its own."""
     gates = list(gates)
-    T = tile if tile else min(m, _lib.SV_FUSED_MAX_TILE)
     out: list[Pass] = []
     i, n = 0, len(gates)
     while i < n:
@@ -67,15 +66,39 @@ def plan_passes(gates, m: int, tile: int = 0) -> list[Pass]:
             while j < n and gates[j].target == t and j - i < _lib.SV_STAGE_MAX_GATES:
                 j += 1
             out.append(Pass("global_stage" if j - i > 1 else "global_gate", tuple(gates[i:j]), t))
-        elif T >= 9 and t < T:
-            while j < n and gates[j].target < T:
-                j += 1
-            out.append(Pass("local_tile" if j - i > 1 else "local_gate", tuple(gates[i:j]), t))
         else:
-            while j < n and gates[j].target == t and j - i < _lib.SV_STAGE_MAX_GATES:
+            while j < n and gates[j].target < m:
                 j += 1
-            out.append(Pass("local_stage" if (j - i > 1 and t >= 5) else "local_gate", tuple(gates[i:j]), t))
+            out.extend(_plan_local(gates[i:j], m, tile))
         i = j
+    return out
+
+
+_GROUP_KIND = {_lib.SV_GROUP_GATES: "local_gate", _lib.SV_GROUP_TILE: "local_tile",
+               _lib.SV_GROUP_STAGE: "local_stage"}
+_KIND_GROUP = {v: k for k, v in _GROUP_KIND.items()}
+
+
+def _plan_local(ops, m: int, tile: int) -> list[Pass]:
+    """Split a run of local-target gates into launch groups with the native planner
+    (sv_plan_gates, the one sv_apply_gates executes).  Rank-bit controls only decide
+    per rank whether a gate applies, so they are planned as uncontrolled."""
+    import ctypes
+
+    arr = (_lib.SvGate * len(ops))()
+    for k, op in enumerate(ops):
+        arr[k].target = op.target
+        arr[k].control = -1 if op.control is None or op.control >= m else op.control
+        arr[k].q[:] = list(_as_gate(op.gate).qbuf())
+    ends = (ctypes.c_int32 * len(ops))()
+    kinds = (ctypes.c_int32 * len(ops))()
+    ng = _lib.load().sv_plan_gates(m, arr, len(ops), int(tile), ends, kinds, len(ops))
+    if ng < 0:
+        _lib.check(ng)
+    out, start = [], 0
+    for g in range(ng):
+        out.append(Pass(_GROUP_KIND[kinds[g]], tuple(ops[start:ends[g]]), ops[start].target))
+        start = ends[g]
     return out
 
 
@@ -98,7 +121,7 @@ def execute_pass(state, p: Pass, transport=None, *, tile: int = 0, executor=None
     if p.local:
         ops = _resolve_rank_controls(p.gates, lay)
         if ops:
-            ex.local_gates(state, ops, tile)
+            ex.local_gates(state, ops, tile, group=_KIND_GROUP[p.kind])
         return
     if transport is None:
         raise LayoutError(f"gate on qubit {p.target} >= m={lay.m} requires a transport")

@@ -58,7 +58,7 @@ class ShmOracleExecutor:
         for op in ops:
             self.exchange(state, theirs, own_is_zero, -1 if op.control is None else op.control, op.gate)
 
-    def local_gates(self, state, ops, tile=0):
+    def local_gates(self, state, ops, tile=0, group=None):
         from oracle import oracle
 
         for op in ops:

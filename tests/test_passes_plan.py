@@ -10,12 +10,28 @@ from paper_1601_07195_b200.passes import _resolve_rank_controls, tile_for
 
 def test_qft_plan_is_one_pass_per_high_stage():
     n, m = 30, 30
-    plan = sv.plan_passes(sv.build_qft(n).gates, m, 12)
+    circ = sv.build_qft(n)
+    plan = sv.plan_passes(circ.gates, m, 12)
     kinds = [p.kind for p in plan]
-    # stages 29..12 each one same-target pass, stages 11..0 one register-tiled run
-    assert kinds == ["local_stage"] * 18 + ["local_tile"]
-    assert [p.target for p in plan[:18]] == list(range(29, 11, -1))
-    assert sum(len(p.gates) for p in plan) == n * (n + 1) // 2
+    # every high transform stage is one same-target pass, the low stages one register-tiled run
+    k = kinds.index("local_tile")
+    assert kinds[:k] == ["local_stage"] * k and kinds[k:] == ["local_tile"] and 18 <= k <= 24
+    assert [p.target for p in plan[:k]] == list(range(29, 29 - k, -1))
+    assert [op for p in plan for op in p.gates] == list(circ.gates)
+
+
+def test_random_circuit_plan_fuses_high_targets():
+    """Tiles gather up to four high qubits: random circuits fuse several gates per pass."""
+    circ = sv.random_circuit(30, 400, np.random.default_rng(1), controlled_fraction=0.3)
+    plan = sv.plan_passes(circ.gates, 30, 12)
+    assert [op for p in plan for op in p.gates] == list(circ.gates)
+    assert len(circ) / len(plan) > 4.0
+    for p in plan:
+        if p.kind == "local_tile":
+            high = {op.target for op in p.gates if op.target >= 8}
+            assert len(high) <= 4
+        if p.kind == "local_stage":
+            assert len({op.target for op in p.gates}) == 1
 
 
 def test_global_stages_and_order_preserved():
@@ -36,10 +52,10 @@ def test_plan_is_rank_independent_and_tile_bounds():
         b = sv.plan_passes(list(circ.gates), m, tile_for(12, m))
         assert a == b
         for p in a:
-            if p.kind == "local_tile":
-                assert all(op.target < 12 for op in p.gates)
+            if p.kind == "local_tile":  # low bits < T-4 plus at most four gathered high bits
+                assert len({op.target for op in p.gates if op.target >= tile_for(12, m) - 4}) <= 4
             if p.kind == "local_stage":
-                assert len({op.target for op in p.gates}) == 1 and p.target >= 12
+                assert len({op.target for op in p.gates}) == 1 and p.target >= 5
     assert tile_for(5, 30) == 0 and tile_for(20, 30) == 13 and tile_for(12, 11) == 11
 
 
