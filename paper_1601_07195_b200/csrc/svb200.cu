@@ -527,8 +527,9 @@ __global__ void __launch_bounds__(1 << (T - TR), (T <= 12) ? 2 : 1)
 constexpr int STAGE_MAX_GATES = 64;
 
 struct StageGate {
-  int32_t control;  // -1: none
+  uint64_t cmask;  // 1 << control; 0: uncontrolled
   int32_t kind;
+  int32_t pad;
   double q[8];
 };
 
@@ -634,22 +635,36 @@ __device__ __forceinline__ bool stage_apply_fast(double2 (&x0)[SUNROLL], double2
   int gi = 0;
   if (SIG == 1) {
     const StageGate &G = P.g[0];
-    const uint64_t cm = G.control >= 0 ? (1ull << G.control) : 0ull;
+    const uint64_t cm = G.cmask;
     if (G.kind == KIND_GENERAL)
       stage_gate_fast<KIND_GENERAL>(x0, x1, ok0, idx, cm, G.q, suspect);
     else if (G.kind == KIND_DIAG)
       stage_gate_fast<KIND_DIAG>(x0, x1, ok0, idx, cm, G.q, suspect);
     else
       stage_gate_fast<KIND_PHASE>(x0, x1, ok0, idx, cm, G.q, suspect);
+    // phases leave x0 alone on the fast path: test it once (conservatively, for
+    // every pair) instead of once per gate
+    bool all0 = true;
+#pragma unroll
+    for (int u = 0; u < SUNROLL; ++u) all0 &= ok0[u];
+    suspect |= !all0;
+#pragma unroll 2
     for (gi = 1; gi < P.ngates; ++gi) {
       const StageGate &H = P.g[gi];
-      stage_gate_fast<KIND_PHASE>(x0, x1, ok0, idx, H.control >= 0 ? (1ull << H.control) : 0ull, H.q, suspect);
+      const uint64_t cm = H.cmask;
+      const double qr = H.q[6], qi = H.q[7];
+#pragma unroll
+      for (int u = 0; u < SUNROLL; ++u) {
+        if (cm && !(idx[u] & cm)) continue;
+        x1[u] = cmul(qr, qi, x1[u]);
+        suspect |= !nonzero2(x1[u]);
+      }
     }
     return suspect;
   }
   for (; gi < P.ngates; ++gi) {
     const StageGate &G = P.g[gi];
-    const uint64_t cm = G.control >= 0 ? (1ull << G.control) : 0ull;
+    const uint64_t cm = G.cmask;
     if (G.kind == KIND_PHASE)
       stage_gate_fast<KIND_PHASE>(x0, x1, ok0, idx, cm, G.q, suspect);
     else if (G.kind == KIND_DIAG)
@@ -671,16 +686,16 @@ __device__ __forceinline__ void stage_apply_exact(double2 (&x0)[SUNROLL], double
   int gi = 0;
   if (SIG == 1) {
     const StageGate &G = P.g[0];
-    stage_gate_any(G.kind, x0, x1, ok0, idx, G.control >= 0 ? (1ull << G.control) : 0ull, G.q);
+    stage_gate_any(G.kind, x0, x1, ok0, idx, G.cmask, G.q);
     for (gi = 1; gi < P.ngates; ++gi) {
       const StageGate &H = P.g[gi];
-      stage_gate<KIND_PHASE, SUNROLL>(x0, x1, ok0, idx, H.control >= 0 ? (1ull << H.control) : 0ull, H.q);
+      stage_gate<KIND_PHASE, SUNROLL>(x0, x1, ok0, idx, H.cmask, H.q);
     }
     return;
   }
   for (; gi < P.ngates; ++gi) {
     const StageGate &G = P.g[gi];
-    stage_gate_any(G.kind, x0, x1, ok0, idx, G.control >= 0 ? (1ull << G.control) : 0ull, G.q);
+    stage_gate_any(G.kind, x0, x1, ok0, idx, G.cmask, G.q);
   }
 }
 
@@ -1101,7 +1116,7 @@ int run_stage(double2 *a, int m, const sv_gate *gates, int n, cudaStream_t st) {
   const int t = gates[0].target;
   P.ngates = n;
   for (int i = 0; i < n; ++i) {
-    P.g[i].control = gates[i].control;
+    P.g[i].cmask = gates[i].control >= 0 ? (1ull << gates[i].control) : 0ull;
     P.g[i].kind = classify_kind(gates[i].q);
     memcpy(P.g[i].q, gates[i].q, sizeof(P.g[i].q));
   }
@@ -1362,7 +1377,7 @@ int sv_exchange_stage(void *mine, void *theirs, int m, int own_is_zero, const sv
   for (int i = 0; i < ngates; ++i) {
     if (gates[i].control < -1 || gates[i].control >= m)
       return fail(SV_EINVAL, "sv_exchange_stage: gate %d control %d is not a local qubit", i, gates[i].control);
-    P.g[i].control = gates[i].control;
+    P.g[i].cmask = gates[i].control >= 0 ? (1ull << gates[i].control) : 0ull;
     P.g[i].kind = classify_kind(gates[i].q);
     memcpy(P.g[i].q, gates[i].q, sizeof(P.g[i].q));
   }
