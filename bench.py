@@ -48,6 +48,9 @@ def parse():
                     help="none: one launch per gate (default, BASELINE config 2 is per-gate); "
                          "passes: native pass planner (default for --workload qft)")
     ap.add_argument("--l-c", type=int, default=12, help="register tile exponent for --fusion passes")
+    ap.add_argument("--data-plane", choices=["ipc", "nccl"], default="ipc",
+                    help="global-qubit exchanges: fused kernel on CUDA-IPC-mapped peer slices (default) or the "
+                         "reference's staged pipeline over NCCL send/recv (baseline)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
@@ -287,7 +290,7 @@ def main():
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=dev)
-        fabric = sv.NvlinkFabric()
+        fabric = sv.NvlinkFabric(data_plane=args.data_plane)
     if world & (world - 1):
         raise SystemExit("--gpus must be a power of two")
     g = world.bit_length() - 1
@@ -447,6 +450,7 @@ def main():
                        "fusion": fusion if fusion == "none" else f"{fusion} (l_c={args.l_c})",
                        "n_qubits": n, "local_qubits": m, "global_qubits": g, "gates_per_step": len(timed[0]),
                        "state_gib_per_gpu": (16 << m) / 2**30, "parallelism": f"state sharded over {world} GPU(s)",
+                       "data_plane": fabric.data_plane if fabric is not None else None,
                        "l2": "no flush: slice >> 126 MB L2" if m >= 26 else "slice fits L2 (parity-size run)",
                        "seed": {"state": 0, "circuit": 1}},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,

@@ -99,6 +99,16 @@ int sv_plan_gates(int m, const sv_gate *gates, int ngates, int tile, int32_t *gr
 /* Execute one planned group (kind SV_GROUP_*), e.g. to time groups one by one. */
 int sv_apply_group(void *amps, int m, int kind, const sv_gate *gates, int ngates, int tile, void *stream);
 
+/* Staged variant of sv_exchange for the NCCL data plane (NvlinkFabric(data_plane=
+ * "nccl"), the reference's chunked pipeline distributed.py:205-290 over NCCL
+ * send/recv): `buf` holds the partner's elements j0 .. j0+count_j-1 of this rank's
+ * computing half (contiguous); the kernel updates mine[] in place and leaves the
+ * partner's updated elements in buf for the return send.  c_local as sv_exchange
+ * but < m-1 (the caller handles the half-selecting bit); j0 and count_j aligned
+ * to 2^(c_local+1). */
+int sv_exchange_chunk(void *mine, void *buf, int m, int own_is_zero, int c_local, const double *q, uint64_t j0,
+                      uint64_t count_j, void *stream);
+
 /* A stage of gates that all target the same global qubit, applied in ONE
  * exchange (sv_exchange generalised to a gate list): each pair crosses NVLink
  * once each way.  Controls must be local (< m) or -1; the caller drops gates

@@ -185,6 +185,28 @@ void or_exchange(double *mine_d, double *theirs_d, int m, int own_is_zero, int c
   }
 }
 
+/* The same update restricted to local indices j0 .. j0+count-1 of the computing
+ * half, with the partner's elements staged contiguously in buf (buf[0] = element
+ * j0): the NCCL data plane's chunk step (distributed.py:257-287). */
+void or_exchange_chunk(double *mine_d, double *buf_d, int m, int own_is_zero, int c_local, const double *q,
+                       int64_t j0, int64_t count) {
+  c128 *mine = (c128 *)mine_d, *buf = (c128 *)buf_d;
+  (void)m;
+  for (int64_t j = j0; j < j0 + count; ++j) {
+    if (c_local >= 0 && !(((uint64_t)j >> c_local) & 1)) continue;
+    c128 a_m = mine[j], a_t = buf[j - j0], keep, ret;
+    if (own_is_zero) {
+      keep = mix(a_m, a_t, q[0], q[1], q[2], q[3]);
+      ret = mix(a_m, a_t, q[4], q[5], q[6], q[7]);
+    } else {
+      keep = mix(a_t, a_m, q[4], q[5], q[6], q[7]);
+      ret = mix(a_t, a_m, q[0], q[1], q[2], q[3]);
+    }
+    mine[j] = keep;
+    buf[j - j0] = ret;
+  }
+}
+
 /* Sum of |a|^2 over the slice, or over bit `qubit` = 1 when qubit >= 0
  * (core.py:147-167).  Reduction order differs from numpy's pairwise sum, so
  * this is compared within tolerance, never bitwise. */

@@ -25,7 +25,8 @@ ABI_VERSION = 1
 
 EXPORTS = (
     "sv_version", "sv_last_error", "sv_launch_count", "sv_apply_single", "sv_apply_controlled",
-    "sv_apply_fused", "sv_apply_gates", "sv_plan_gates", "sv_apply_group", "sv_exchange", "sv_exchange_stage","sv_norm_sq", "sv_init_random", "sv_scale", "sv_init_basis",
+    "sv_apply_fused", "sv_apply_gates", "sv_plan_gates", "sv_apply_group", "sv_exchange", "sv_exchange_chunk",
+    "sv_exchange_stage","sv_norm_sq", "sv_init_random", "sv_scale", "sv_init_basis",
     "sv_copy", "sv_ipc_handle", "sv_ipc_open", "sv_ipc_close",
 )
 
@@ -68,6 +69,7 @@ def load() -> ctypes.CDLL:
                            ctypes.POINTER(ctypes.c_int32), i], i),
         "sv_apply_group": ([vp, i, i, ctypes.POINTER(SvGate), i, i, vp], i),
         "sv_exchange": ([vp, vp, i, i, i, dp, vp], i),
+        "sv_exchange_chunk": ([vp, vp, i, i, i, dp, u64, u64, vp], i),
         "sv_exchange_stage": ([vp, vp, i, i, ctypes.POINTER(SvGate), i, vp], i),
         "sv_norm_sq": ([vp, i, i, vp, vp], i),
         "sv_init_random": ([vp, i, u64, u64, vp], i),

@@ -1415,6 +1415,25 @@ int sv_exchange(void *mine, void *theirs, int m, int own_is_zero, int c_local, c
   return after_launch("sv_exchange");
 }
 
+int sv_exchange_chunk(void *mine, void *buf, int m, int own_is_zero, int c_local, const double *q, uint64_t j0,
+                      uint64_t count_j, void *stream) {
+  if (bad_ptr(mine) || bad_ptr(buf) || !q) return fail(SV_EINVAL, "sv_exchange_chunk: null or misaligned pointer");
+  if (m < 1 || m > 62) return fail(SV_EINVAL, "sv_exchange_chunk: m=%d out of range", m);
+  if (c_local < -1 || c_local >= m - 1)
+    return fail(SV_EINVAL, "sv_exchange_chunk: control %d not an interior local bit (m=%d)", c_local, m);
+  const uint64_t half = 1ull << (m - 1), lo = own_is_zero ? 0 : half;
+  if (count_j == 0) return SV_OK;
+  if (j0 < lo || j0 + count_j > lo + half) return fail(SV_EINVAL, "sv_exchange_chunk: range outside own half");
+  const uint64_t align = c_local >= 0 ? (2ull << c_local) : 1ull;
+  if (j0 % align || count_j % align) return fail(SV_EINVAL, "sv_exchange_chunk: range not aligned to 2^(c+1)");
+  const uint64_t count = c_local >= 0 ? count_j >> 1 : count_j;
+  // k_exchange addresses theirs[j]: shift the chunk buffer so that buf[0] is element j0
+  double2 *theirs = (double2 *)buf - j0;
+  k_exchange<<<grid_for(count, BLK * UNROLL), BLK, 0, (cudaStream_t)stream>>>(
+      (double2 *)mine, theirs, count, j0, c_local, own_is_zero ? 1 : 0, load_q(q));
+  return after_launch("sv_exchange_chunk");
+}
+
 int sv_norm_sq(const void *amps, int m, int qubit, double *scratch, void *stream) {
   if (bad_ptr(amps) || !scratch) return fail(SV_EINVAL, "sv_norm_sq: null or misaligned pointer");
   if (m < 0 || m > 62) return fail(SV_EINVAL, "sv_norm_sq: m=%d out of range", m);

@@ -207,6 +207,19 @@ class CudaExecutor:
             _lib.check(_lib.load().sv_exchange(ptr, theirs, m, int(own_is_zero), int(c_local),
                                                _as_gate(q).qbuf(), stream_handle()))
 
+    def exchange_chunk(self, state: LocalState, buf: torch.Tensor, own_is_zero: bool, c_local: int, q: GateMatrix,
+                       j0: int, count: int) -> None:
+        ptr, m = device_view(state.amps)
+        with torch.cuda.device(state.amps.device):
+            _lib.check(_lib.load().sv_exchange_chunk(ptr, buf.data_ptr(), m, int(own_is_zero), int(c_local),
+                                                     _as_gate(q).qbuf(), j0, count, stream_handle()))
+
+    def scratch(self, state: LocalState, num_amps: int) -> torch.Tensor:
+        return torch.empty(num_amps, dtype=torch.complex128, device=state.amps.device)
+
+    def view(self, state: LocalState, j0: int, num_amps: int) -> torch.Tensor:
+        return state.amps[j0:j0 + num_amps]
+
     def exchange_stage(self, state: LocalState, theirs: int, own_is_zero: bool, ops) -> None:
         from .kernels import gate_array
 
@@ -270,7 +283,8 @@ class NvlinkFabric:
     follow CountingTransport: payload bytes sent / received over the link.
     """
 
-    def __init__(self, group=None, *, fence: str | None = None, executor=None):
+    def __init__(self, group=None, *, fence: str | None = None, executor=None, data_plane: str = "ipc",
+                 chunk_amps: int = 1 << 26):
         import torch.distributed as dist
 
         if not dist.is_initialized():
@@ -283,6 +297,14 @@ class NvlinkFabric:
         self.fence_mode = fence or ("stream" if backend == "nccl" else "host")
         if self.fence_mode not in ("stream", "host"):
             raise ValueError("fence must be 'stream' or 'host'")
+        if data_plane not in ("ipc", "nccl"):
+            raise ValueError("data_plane must be 'ipc' or 'nccl'")
+        # "ipc": fused kernel on the partner's mapped slice (the product).  "nccl": the
+        # reference's staged pipeline over send/recv (baseline, and the fallback when
+        # peer mapping is refused); switched collectively in ensure_registered.
+        self.data_plane = data_plane
+        self.chunk_amps = chunk_amps
+        self._scratch: torch.Tensor | None = None
         self.executor = executor or _CUDA
         self.sent_bytes = 0
         self.received_bytes = 0
@@ -336,16 +358,93 @@ class NvlinkFabric:
 
     # --- peer mappings
     def ensure_registered(self, state: LocalState) -> None:
-        """Collective: map every rank's slice into this process (once per slice)."""
+        """Collective: map every rank's slice into this process (once per slice).
+
+        If any rank cannot export or map a slice, every rank drops its mappings and
+        switches to the NCCL data plane together (the decision is all-gathered, so
+        the ranks never disagree on the protocol)."""
+        if self.data_plane == "nccl":
+            return
         key = self.executor.key(state)
         if key in self._peers:
             return
-        blobs = self.exchange_objects(self.executor.share(state))
+        err = None
+        try:
+            mine = self.executor.share(state)
+        except Exception as exc:  # noqa: BLE001 -- reported below, collectively
+            mine, err = None, exc
+        blobs = self.exchange_objects(mine)
         ptrs = [None] * self.num_ranks
-        for r, blob in enumerate(blobs):
-            if r != self.rank:
-                ptrs[r] = self.executor.open(state, blob)
-        self._peers[key] = (ptrs, blobs)
+        if err is None and all(b is not None for b in blobs):
+            for r, blob in enumerate(blobs):
+                if r != self.rank:
+                    try:
+                        ptrs[r] = self.executor.open(state, blob)
+                    except Exception as exc:  # noqa: BLE001
+                        err = exc
+                        break
+        ok = self.exchange_objects(err is None)
+        if all(ok):
+            self._peers[key] = (ptrs, blobs)
+            return
+        for r, p in enumerate(ptrs):
+            if p is not None:
+                self.executor.close(p, blobs[r])
+        import warnings
+
+        warnings.warn(f"peer mapping refused on some rank ({err!r} here); exchanges fall back to NCCL send/recv")
+        self.data_plane = "nccl"
+
+    def nccl_exchange(self, state: LocalState, action: GateAction, q: GateMatrix) -> int:
+        """The reference's half exchange over send/recv (distributed.py:205-311), staged in
+        chunks through one scratch buffer.  Returns payload bytes sent (== received).
+
+        Stage s covers half s; its computing rank (zero side for s = 0) receives the
+        partner's chunk, updates both with sv_exchange_chunk and sends the partner's
+        updated elements back; the passive rank sends its chunk and receives it
+        updated, straight into its slice.  Case 5 moves whole chunks (the kernel
+        updates only local-bit-c elements)."""
+        dist = self._dist
+        ex = self.executor
+        m = state.layout.m
+        half = 1 << (m - 1)
+        chunk = min(self.chunk_amps, half)
+        peer = action.partner if self.group is None else dist.get_global_rank(self.group, action.partner)
+        moved = 0
+        for stage in (0, 1):
+            c_local = action.c_local
+            if c_local == m - 1:  # the half-selecting bit: only the second half holds control-set pairs
+                if stage == 0:
+                    continue
+                c_local = -1
+            computing = action.own_is_zero == (stage == 0)
+            if computing and (self._scratch is None or self._scratch.numel() < chunk):
+                self._scratch = ex.scratch(state, chunk)
+            for j0 in range(stage * half, (stage + 1) * half, chunk):
+                if computing:
+                    buf = self._scratch[:chunk]
+                    self._recv(buf, peer)
+                    ex.exchange_chunk(state, buf, action.own_is_zero, c_local, q, j0, chunk)
+                    self._send(buf, peer)
+                else:
+                    view = ex.view(state, j0, chunk)
+                    self._send(view, peer)
+                    self._recv(view, peer)
+                moved += chunk * AMP_BYTES
+        return moved
+
+    def _send(self, t: torch.Tensor, peer: int) -> None:
+        if t.is_cuda and self.fence_mode == "host":  # gloo moves host memory only
+            t = t.cpu()
+        self._dist.send(t, dst=peer, group=self.group)
+
+    def _recv(self, t: torch.Tensor, peer: int) -> None:
+        if t.is_cuda and self.fence_mode == "host":
+            tmp = torch.empty(t.shape, dtype=t.dtype)
+            self._dist.recv(tmp, src=peer, group=self.group)
+            t.copy_(tmp)
+            return
+        self._dist.recv(t, src=peer, group=self.group)
 
     def peer_pointer(self, state: LocalState, rank: int) -> int:
         key = self.executor.key(state)
@@ -392,9 +491,14 @@ def execute_action(state: LocalState, action: GateAction, q: GateMatrix, fabric:
         # Partner slices are read and written in place: every rank's prior
         # work must be complete before, and the exchange complete after.
         fabric.barrier(state)
-        if action.kind == "exchange":
-            ex.exchange(state, fabric.peer_pointer(state, action.partner), action.own_is_zero, action.c_local, q)
-        fabric.count(action.sent, action.received)
+        if action.kind == "exchange" and getattr(fabric, "data_plane", "ipc") == "nccl":
+            moved = fabric.nccl_exchange(state, action, q)
+            fabric.count(moved, moved)
+        else:
+            if action.kind == "exchange":
+                ex.exchange(state, fabric.peer_pointer(state, action.partner), action.own_is_zero, action.c_local,
+                            q)
+            fabric.count(action.sent, action.received)
         fabric.barrier(state)
     except BaseException:
         state.corrupt = True
@@ -505,12 +609,19 @@ def gather_full_state(state: LocalState, transport: NvlinkFabric | None = None,
     transport.ensure_registered(state)
     transport.barrier(state)
     full = None
+    nccl = getattr(transport, "data_plane", "ipc") == "nccl"
     if lay.rank == 0:
         dev = torch.empty(1 << lay.n, dtype=torch.complex128, device=state.amps.device)
         nbytes = lay.local_len * AMP_BYTES
         dev[: lay.local_len].copy_(state.amps)
         for src in range(1, lay.num_ranks):
-            transport.executor.copy(dev[src << lay.m:].data_ptr(), transport.peer_pointer(state, src), nbytes, state)
+            if nccl:
+                transport._recv(dev[src << lay.m:(src + 1) << lay.m], src)
+            else:
+                transport.executor.copy(dev[src << lay.m:].data_ptr(), transport.peer_pointer(state, src), nbytes,
+                                        state)
         full = dev.cpu().numpy()
+    elif nccl:
+        transport._send(state.amps, 0)
     transport.barrier(state)
     return full

@@ -27,7 +27,8 @@ from dataclasses import dataclass
 
 from . import _lib
 from .circuits import GateOp
-from .distributed import _CUDA, _check_transport, apply_global
+from .distributed import _CUDA, GateAction, _check_transport, apply_global
+from .perfmodel import BoundCase
 from .errors import LayoutError
 from .kernels import _as_gate
 
@@ -139,7 +140,13 @@ def execute_pass(state, p: Pass, transport=None, *, tile: int = 0, executor=None
            for op in _resolve_rank_controls(p.gates, lay)]
     try:
         transport.barrier(state)
-        if ops:
+        if ops and getattr(transport, "data_plane", "ipc") == "nccl":
+            for op in ops:  # staged fallback: one send/recv exchange per gate of the stage
+                act = GateAction("exchange", BoundCase.SINGLE_REMOTE, op.target, op.control, partner=partner,
+                                 own_is_zero=zero, c_local=-1 if op.control is None else op.control)
+                moved = transport.nccl_exchange(state, act, op.gate)
+                transport.count(moved, moved)
+        elif ops:
             ex.exchange_stage(state, transport.peer_pointer(state, partner), zero, ops)
             transport.count(1 << (lay.m + 4), 1 << (lay.m + 4))
         transport.barrier(state)

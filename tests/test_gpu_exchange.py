@@ -38,6 +38,7 @@ class LoopbackFabric:
     def __init__(self, states, rank):
         self.states, self.rank, self.num_ranks = states, rank, len(states)
         self.executor = sv.CudaExecutor()
+        self.data_plane = "ipc"
         self.sent_bytes = self.received_bytes = 0
         self._tag = 0
 
@@ -133,6 +134,38 @@ def test_exchange_abi_rejects_bad_arguments():
     assert L.sv_exchange(a.data_ptr(), 0, 4, 1, -1, q, st) == _lib.SV_EINVAL
 
 
+@pytest.mark.parametrize("c_local", [-1, 0, 2, 5])
+def test_exchange_chunk_staged_protocol(c_local):
+    """The NCCL data plane's chunk step, with the send/recv replaced by device copies."""
+    from paper_1601_07195_b200 import _lib
+
+    n, m = 12, 11
+    rng = np.random.default_rng(40 + c_local)
+    v = random_state(rng, n)
+    q = sv.random_unitary(rng)
+    want = v.copy()
+    if c_local < 0:
+        oracle.apply_single(want, n - 1, q)
+    else:
+        oracle.apply_controlled(want, c_local, n - 1, q)
+    ranks = [torch.from_numpy(v[: 1 << m].copy()).to(DEV), torch.from_numpy(v[1 << m:].copy()).to(DEV)]
+    half, chunk = 1 << (m - 1), 1 << (m - 3)
+    L = _lib.load()
+    st = torch.cuda.current_stream().cuda_stream
+    for stage in (0, 1):
+        comp, pas = ranks[stage], ranks[1 - stage]  # zero side computes the first half
+        for j0 in range(stage * half, (stage + 1) * half, chunk):
+            buf = pas[j0:j0 + chunk].clone()          # "recv" the partner's chunk
+            _lib.check(L.sv_exchange_chunk(comp.data_ptr(), buf.data_ptr(), m, int(stage == 0), c_local, q.qbuf(),
+                                           j0, chunk, st))
+            pas[j0:j0 + chunk].copy_(buf)             # "send" it back
+    torch.cuda.synchronize()
+    assert np.array_equal(np.concatenate([r.cpu().numpy() for r in ranks]), want)
+    with pytest.raises(ValueError):
+        _lib.check(L.sv_exchange_chunk(ranks[0].data_ptr(), buf.data_ptr(), m, 1, c_local if c_local > 0 else 1,
+                                       q.qbuf(), 1, chunk, st))  # misaligned start
+
+
 # --------------------------------------------------- two processes, real IPC
 
 
@@ -142,7 +175,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _ipc_worker(rank, world, port, path, n, seed):
+def _ipc_worker(rank, world, port, path, n, plane):
     import torch.distributed as dist
 
     import paper_1601_07195_b200 as svm
@@ -152,7 +185,7 @@ def _ipc_worker(rank, world, port, path, n, seed):
     try:
         p = world.bit_length() - 1
         d = dict(np.load(path + ".in.npz"))
-        fabric = svm.NvlinkFabric(fence="host")
+        fabric = svm.NvlinkFabric(fence="host", data_plane=plane, chunk_amps=1 << 7)
         circ = svm.Circuit(n, [svm.GateOp(svm.GateMatrix.unchecked(q.reshape(2, 2)), int(t),
                                           None if c < 0 else int(c)) for t, c, q in zip(d["t"], d["c"], d["q"])])
         st = svm.state_from_global(svm.Layout(n, p, rank), d["init"], device="cuda:0")
@@ -167,7 +200,8 @@ def _ipc_worker(rank, world, port, path, n, seed):
         dist.destroy_process_group()
 
 
-def test_two_process_ipc_fabric_matches_oracle():
+@pytest.mark.parametrize("plane", ["ipc", "nccl"])
+def test_two_process_ipc_fabric_matches_oracle(plane):
     import torch.multiprocessing as mp
 
     n, world = 12, 2
@@ -183,7 +217,7 @@ def test_two_process_ipc_fabric_matches_oracle():
         np.savez(path + ".in.npz", init=init, t=np.array([o.target for o in circ]),
                  c=np.array([-1 if o.control is None else o.control for o in circ]),
                  q=np.stack([o.gate.mat.reshape(4) for o in circ]))
-        mp.spawn(_ipc_worker, args=(world, _free_port(), path, n, 0), nprocs=world, join=True)
+        mp.spawn(_ipc_worker, args=(world, _free_port(), path, n, plane), nprocs=world, join=True)
         out = dict(np.load(path + ".out.npz"))
     assert np.array_equal(out["full"], want)
     assert abs(float(out["norm"]) - 1.0) < 1e-12
