@@ -657,7 +657,9 @@ __device__ __forceinline__ bool stage_apply_fast(double2 (&x0)[SUNROLL], double2
       for (int u = 0; u < SUNROLL; ++u) {
         if (cm && !(idx[u] & cm)) continue;
         x1[u] = cmul(qr, qi, x1[u]);
-        suspect |= !nonzero2(x1[u]);
+        // zero test on the FP64 pipe (DSETP, predicate-accumulated): the ALU pipe is the
+        // busier one here.  x != 0.0 is false exactly for +-0 (NaN, subnormals count as nonzero).
+        suspect |= (x1[u].x == 0.0) | (x1[u].y == 0.0);
       }
     }
     return suspect;
