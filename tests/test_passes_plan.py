@@ -59,6 +59,51 @@ def test_plan_is_rank_independent_and_tile_bounds():
     assert tile_for(5, 30) == 0 and tile_for(20, 30) == 13 and tile_for(12, 11) == 11
 
 
+from hypothesis import given, settings  # noqa: E402
+from hypothesis import strategies as st  # noqa: E402
+
+
+@given(st.integers(9, 34), st.integers(0, 2**31 - 1), st.sampled_from([0, 9, 12, 13]))
+@settings(max_examples=60, deadline=None)
+def test_native_planner_invariants(m, seed, tile):
+    """sv_plan_gates (the planner sv_apply_gates runs): order-preserving cover, one launch per
+    group, tile groups gather at most four bits above T-4, stages share one target >= 5."""
+    rng = np.random.default_rng(seed)
+    T = tile if tile and tile <= min(m, 13) else min(m, 13)
+    zoo = [sv.hadamard(), sv.phase_r(3), sv.pauli_z(), sv.random_unitary(rng)]
+    ops = []
+    for _ in range(int(rng.integers(1, 400))):
+        t = int(rng.integers(m)) if rng.random() < 0.7 else int(rng.integers(min(m, 6)))
+        c = None if rng.random() < 0.5 else int((t + 1 + rng.integers(m - 1)) % m)
+        ops.append(sv.GateOp(zoo[int(rng.integers(4))], t, c))
+    plan = sv.plan_passes(ops, m, T if tile else 0)
+    assert [op for p in plan for op in p.gates] == ops
+    for p in plan:
+        targets = {op.target for op in p.gates}
+        if p.kind == "local_tile":
+            assert len(p.gates) <= sv._lib.SV_FUSED_MAX_GATES
+            assert len({t for t in targets if t >= T - 4}) <= 4
+        elif p.kind == "local_stage":
+            assert len(targets) == 1 and p.target >= 5 and len(p.gates) <= sv._lib.SV_STAGE_MAX_GATES
+        else:
+            assert p.kind == "local_gate"
+
+
+def test_planner_abi_errors():
+    import ctypes
+
+    from paper_1601_07195_b200 import _lib
+
+    L = _lib.load()
+    g = sv.kernels.gate_array([sv.GateOp(sv.hadamard(), 3)])
+    ends = (ctypes.c_int32 * 4)()
+    kinds = (ctypes.c_int32 * 4)()
+    assert L.sv_plan_gates(3, g, 1, 0, ends, kinds, 4) == _lib.SV_EINVAL   # target 3 not local at m=3
+    assert L.sv_plan_gates(20, g, 1, 14, ends, kinds, 4) == _lib.SV_EINVAL  # tile out of range
+    assert L.sv_plan_gates(20, g, 1, 0, ends, kinds, 4) == 1 and kinds[0] == _lib.SV_GROUP_GATES
+    assert L.sv_apply_group(None, 20, 1, g, 1, 0, None) == _lib.SV_EINVAL
+
+
 def test_rank_controls_resolve_per_rank():
     lay0, lay1 = sv.Layout(8, 1, 0), sv.Layout(8, 1, 1)
     ops = [sv.GateOp(sv.hadamard(), 2, 7), sv.GateOp(sv.hadamard(), 3, 1), sv.GateOp(sv.hadamard(), 4)]
