@@ -11,6 +11,7 @@ streams only, every update is a libsvb200 kernel.
 
 from __future__ import annotations
 
+import itertools
 from dataclasses import dataclass, field
 from typing import TYPE_CHECKING
 
@@ -26,6 +27,7 @@ if TYPE_CHECKING:
 
 AMP_BYTES = 16
 ALIGNMENT = 64
+_UIDS = itertools.count(1)
 
 
 @dataclass(frozen=True)
@@ -88,6 +90,9 @@ class LocalState:
     layout: Layout
     amps: torch.Tensor
     corrupt: bool = field(default=False, compare=False)
+    # process-unique id: peer mappings are keyed by it, so a new slice that happens to
+    # reuse a freed slice's address never inherits that slice's stale mappings
+    uid: int = field(default_factory=lambda: next(_UIDS), compare=False, repr=False)
 
     def __post_init__(self):
         if not isinstance(self.amps, torch.Tensor) or self.amps.dtype != torch.complex128:

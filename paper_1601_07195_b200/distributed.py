@@ -244,7 +244,7 @@ class CudaExecutor:
         torch.cuda.current_stream(state.amps.device).synchronize()
 
     def key(self, state: LocalState) -> tuple:
-        return (state.amps.data_ptr(), state.amps.numel(), str(state.amps.device))
+        return (getattr(state, "uid", None), state.amps.data_ptr(), state.amps.numel(), str(state.amps.device))
 
     def flag_device(self, state: LocalState | None) -> torch.device:
         return state.amps.device if state is not None else torch.device("cuda", torch.cuda.current_device())
