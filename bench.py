@@ -300,6 +300,9 @@ def main():
     fusion = args.fusion or ("passes" if args.workload == "qft" else "none")
     circs = step_circuits(sv, args.workload, n, args.warmup + args.steps)
     state = sv.init_random_state(lay, seed=0, transport=fabric, device=dev)
+    # full-size self-check: keep the initial slice, undo every step at the end
+    free_b, _ = torch.cuda.mem_get_info(dev)
+    initial = state.amps.clone() if free_b > 5 * (16 << lay.m) else None
     stream = torch.cuda.current_stream()
     fcfg = sv.FusionConfig(l_c=args.l_c, passes=True) if fusion == "passes" else None
 
@@ -401,6 +404,20 @@ def main():
                   "frac_nominal": round(per_dir / (d * 1e-3) / 1e9 / 900.0, 4),
                   "global_launches_per_step": len(glob) // len(timed), "avg_ms": round(d, 3)}
 
+    # ------------------------------ self-check: inverse circuits restore the input
+    self_check = None
+    if initial is not None:
+        for c in reversed(circs):
+            sv.run_circuit(state, c.inverse(), fabric, fusion=fcfg)
+        err = float((state.amps - initial).abs().max().item())
+        if world > 1:
+            err = reduce_scalar(err, dist.ReduceOp.MAX)
+        ng = 2 * sum(len(c) for c in circs)
+        self_check = {"max_abs_err": err, "bound": 1e-12 * ng ** 0.5, "gates": ng,
+                      "ok": err <= 1e-12 * ng ** 0.5,
+                      "what": "every warm-up and timed step undone by its inverse circuit, vs the saved input"}
+        del initial
+
     # ---------------------------------------------- end to end (host buffers)
     e2e = None
     cpu = None
@@ -453,7 +470,7 @@ def main():
                        "data_plane": fabric.data_plane if fabric is not None else None,
                        "l2": "no flush: slice >> 126 MB L2" if m >= 26 else "slice fits L2 (parity-size run)",
                        "seed": {"state": 0, "circuit": 1}},
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "self_check": self_check,
             "clocks": clocks.summary(),
         }
         if buckets:
