@@ -648,11 +648,26 @@ __device__ __forceinline__ bool stage_apply_fast(double2 (&x0)[SUNROLL], double2
 #pragma unroll
     for (int u = 0; u < SUNROLL; ++u) all0 &= ok0[u];
     suspect |= !all0;
+    // The pairs of a thread differ only in the index bits that separate the unrolled
+    // rows; any other control bit has the same value for all of them, so one test
+    // (on a 32-bit word when it can) decides the whole row set.
+    uint64_t rows = 0;
+#pragma unroll
+    for (int u = 1; u < SUNROLL; ++u) rows |= idx[u] ^ idx[0];
 #pragma unroll 2
     for (gi = 1; gi < P.ngates; ++gi) {
       const StageGate &H = P.g[gi];
       const uint64_t cm = H.cmask;
       const double qr = H.q[6], qi = H.q[7];
+      if (cm && !(cm & rows)) {
+        if (!(idx[0] & cm)) continue;
+#pragma unroll
+        for (int u = 0; u < SUNROLL; ++u) {
+          x1[u] = cmul(qr, qi, x1[u]);
+          suspect |= (x1[u].x == 0.0) | (x1[u].y == 0.0);
+        }
+        continue;
+      }
 #pragma unroll
       for (int u = 0; u < SUNROLL; ++u) {
         if (cm && !(idx[u] & cm)) continue;
