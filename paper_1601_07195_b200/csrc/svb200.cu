@@ -361,23 +361,23 @@ __device__ __forceinline__ int reg_off(int j, const int m0, const int m1, const 
 // branch (see stage_gate).  FULL: every pair active (pm == 0xFFFF).
 constexpr int TG = 2;
 
-// SPEC (speculative) variant: diagonal/phase gates update in place with their
-// products only and raise `suspect` on any zero component; the kernel then
-// replays the whole tile from global memory with the exact variant (k_tile).
-template <int TB, int KIND, bool FULL, bool SPEC>
-__device__ __forceinline__ void tile_gate_k(double2 (&r)[TRN], uint32_t pm, const double *qp, bool &suspect) {
+// spec (speculative pass, warp-uniform): diagonal/phase gates update in place
+// with their products only; k_tile tests the final tile once and replays it
+// from global memory with spec = false if any component is zero (see
+// stage_gate_fast for why that one test is enough).
+template <int TB, int KIND, bool FULL>
+__device__ __forceinline__ void tile_gate_k(double2 (&r)[TRN], uint32_t pm, const double *qp, bool spec) {
   double q[8];  // once per gate in registers, not one constant-bank load per pair
 #pragma unroll
   for (int i = 0; i < 8; ++i) q[i] = qp[i];
 #define PAIRS(k) ((((k) >> TB) << (TB + 1)) | ((k) & ((1 << TB) - 1)))  // k-th j with bit TB clear
-  if (SPEC && KIND != KIND_GENERAL) {
+  if (KIND != KIND_GENERAL && spec) {
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const int j = PAIRS(k);
       if (!(FULL || ((pm >> j) & 1u))) continue;
       if (KIND == KIND_DIAG) r[j] = cmul(q[0], q[1], r[j]);
       r[j | (1 << TB)] = cmul(q[6], q[7], r[j | (1 << TB)]);
-      suspect |= !(nonzero2(r[j]) & nonzero2(r[j | (1 << TB)]));
     }
     return;
   }
@@ -420,32 +420,31 @@ __device__ __forceinline__ void tile_gate_k(double2 (&r)[TRN], uint32_t pm, cons
   }
 }
 
-template <int TB, bool SPEC>
-__device__ __forceinline__ void tile_gate(double2 (&r)[TRN], uint32_t pm, int kind, const double *q, bool &sus) {
+template <int TB>
+__device__ __forceinline__ void tile_gate(double2 (&r)[TRN], uint32_t pm, int kind, const double *q, bool spec) {
   if (pm == 0u) return;
   if (pm == 0xFFFFu) {  // uncontrolled, or control decided per thread/CTA: straight-line code
     if (kind == KIND_GENERAL)
-      tile_gate_k<TB, KIND_GENERAL, true, SPEC>(r, pm, q, sus);
+      tile_gate_k<TB, KIND_GENERAL, true>(r, pm, q, spec);
     else if (kind == KIND_PHASE)
-      tile_gate_k<TB, KIND_PHASE, true, SPEC>(r, pm, q, sus);
+      tile_gate_k<TB, KIND_PHASE, true>(r, pm, q, spec);
     else
-      tile_gate_k<TB, KIND_DIAG, true, SPEC>(r, pm, q, sus);
+      tile_gate_k<TB, KIND_DIAG, true>(r, pm, q, spec);
     return;
   }
   if (kind == KIND_GENERAL)
-    tile_gate_k<TB, KIND_GENERAL, false, SPEC>(r, pm, q, sus);
+    tile_gate_k<TB, KIND_GENERAL, false>(r, pm, q, spec);
   else if (kind == KIND_PHASE)
-    tile_gate_k<TB, KIND_PHASE, false, SPEC>(r, pm, q, sus);
+    tile_gate_k<TB, KIND_PHASE, false>(r, pm, q, spec);
   else
-    tile_gate_k<TB, KIND_DIAG, false, SPEC>(r, pm, q, sus);
+    tile_gate_k<TB, KIND_DIAG, false>(r, pm, q, spec);
 }
 
 // One tile through the run: load (natural layout), segments with transposes,
 // back to the natural layout in registers (the caller stores).
-template <int T, bool SPEC>
+template <int T>
 __device__ __forceinline__ void tile_body(const double2 *__restrict__ a, uint64_t tile0, const int (&hb)[TR],
-                                          int tid, const TileParams &P, double2 *s, double2 (&r)[TRN],
-                                          bool &suspect) {
+                                          int tid, const TileParams &P, double2 *s, double2 (&r)[TRN], bool spec) {
   constexpr int NT = 1 << (T - TR);
 #pragma unroll
   for (int j = 0; j < TRN; ++j) r[j] = a[tile0 + tile_off<T>(tid, j, hb)];
@@ -479,10 +478,10 @@ __device__ __forceinline__ void tile_body(const double2 *__restrict__ a, uint64_
       else if (G.cmode == 3)
         pm = ((tile0 >> G.cabove) & 1ull) ? 0xFFFFu : 0u;
       switch (G.tb) {
-        case 0: tile_gate<0, SPEC>(r, pm, G.kind, G.q, suspect); break;
-        case 1: tile_gate<1, SPEC>(r, pm, G.kind, G.q, suspect); break;
-        case 2: tile_gate<2, SPEC>(r, pm, G.kind, G.q, suspect); break;
-        default: tile_gate<3, SPEC>(r, pm, G.kind, G.q, suspect); break;
+        case 0: tile_gate<0>(r, pm, G.kind, G.q, spec); break;
+        case 1: tile_gate<1>(r, pm, G.kind, G.q, spec); break;
+        case 2: tile_gate<2>(r, pm, G.kind, G.q, spec); break;
+        default: tile_gate<3>(r, pm, G.kind, G.q, spec); break;
       }
     }
   }
@@ -496,13 +495,28 @@ __device__ __forceinline__ void tile_body(const double2 *__restrict__ a, uint64_
   }
 }
 
-// SPEC = true when the run holds diagonal/phase gates (host-chosen): speculative
-// in-place updates, and on any zero component the whole tile is replayed
-// exactly from global memory (nothing stored yet).  SPEC = false: exact path.
+// The exact replay of one tile (rare: a zero component in the speculative
+// result).  Out of line, so the hot kernel does not carry a second copy of
+// the body in its register allocation (inlined, the pair spilled ~3 KB per
+// thread at the 128-register cap); the call site keeps only a few scalars live.
+template <int T>
+__device__ __noinline__ void tile_replay(double2 *__restrict__ a, uint64_t tile0, int hb0, int hb1, int hb2,
+                                         int hb3, const TileParams *P, double2 *s) {
+  const int hb[TR] = {hb0, hb1, hb2, hb3};
+  const int tid = threadIdx.x;
+  double2 r[TRN];
+  tile_body<T>(a, tile0, hb, tid, *P, s, r, false);
+#pragma unroll
+  for (int j = 0; j < TRN; ++j) a[tile0 + tile_off<T>(tid, j, hb)] = r[j];
+}
+
+// SPEC = true when the run is mostly diagonal/phase gates (host-chosen):
+// speculative in-place updates, one zero test of the final tile, and on any
+// zero component the whole tile is replayed exactly from global memory
+// (nothing has been stored yet).  SPEC = false: the exact path.
 template <int T, bool SPEC>
 __global__ void __launch_bounds__(1 << (T - TR), (T <= 12) ? 2 : 1)
-    k_tile(double2 *__restrict__ a, const TileParams P) {
-  constexpr int NT = 1 << (T - TR);
+    k_tile(double2 *__restrict__ a, const __grid_constant__ TileParams P) {
   extern __shared__ double2 s[];
   int hb[TR];
 #pragma unroll
@@ -510,12 +524,18 @@ __global__ void __launch_bounds__(1 << (T - TR), (T <= 12) ? 2 : 1)
   const uint64_t tile0 = tile_base<T>(blockIdx.x, hb);  // every non-tile slice bit of this CTA
   const int tid = threadIdx.x;
   double2 r[TRN];
-  bool suspect = false;
-  tile_body<T, SPEC>(a, tile0, hb, tid, P, s, r, suspect);
-  if (SPEC && __syncthreads_or(suspect)) tile_body<T, false>(a, tile0, hb, tid, P, s, r, suspect);
+  tile_body<T>(a, tile0, hb, tid, P, s, r, SPEC);
+  if (SPEC) {
+    bool ok = true;
+#pragma unroll
+    for (int j = 0; j < TRN; ++j) ok &= nonzero2(r[j]);
+    if (__syncthreads_or(!ok)) {
+      tile_replay<T>(a, tile0, hb[0], hb[1], hb[2], hb[3], &P, s);
+      return;
+    }
+  }
 #pragma unroll
   for (int j = 0; j < TRN; ++j) a[tile0 + tile_off<T>(tid, j, hb)] = r[j];
-  (void)NT;
 }
 
 // ------------------------------------------------------------ same-target stages
@@ -595,16 +615,20 @@ __device__ __forceinline__ void stage_gate_any(int kind, double2 (&x0)[SUNROLL],
 }
 
 // Speculative fast path: general gates run the full mix(); diagonal and phase
-// gates update in place with their products only and raise `suspect` on any
-// zero component (the one case where the skipped signed-zero term of mix() can
-// change a bit).  The kernels store nothing until the stage is done, so a
-// suspect thread reloads its pairs from memory and replays the stage through
-// stage_apply_exact.  No per-gate branch and no register copies on the common
-// path.
+// gates update in place with their products only.  The result is tested ONCE,
+// after the whole stage:
+//   Dropping the zero-matrix terms of mix() only ever changes the sign of a
+//   zero: cmul(0, a) is a signed zero and x + (+-0) == x for x != 0.  And
+//   values that agree up to the signs of their zeros stay that way through
+//   any later mul/fma/add (a +-0 operand gives a +-0 product, which again only
+//   matters when the other addend is zero).  So the fast path's final pairs
+//   equal the exact ones except possibly where a final component is +-0.
+// A thread with any zero component in its final pairs reloads them (nothing is
+// stored before the stage is done) and replays the stage through
+// stage_apply_exact; everyone else stores the fast result.  No per-gate tests.
 template <int KIND>
 __device__ __forceinline__ void stage_gate_fast(double2 (&x0)[SUNROLL], double2 (&x1)[SUNROLL],
-                                                bool (&ok0)[SUNROLL], const uint64_t (&idx)[SUNROLL],
-                                                uint64_t cm, const double *qp, bool &suspect) {
+                                                const uint64_t (&idx)[SUNROLL], uint64_t cm, const double *qp) {
   double q[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) q[i] = qp[i];
@@ -613,15 +637,11 @@ __device__ __forceinline__ void stage_gate_fast(double2 (&x0)[SUNROLL], double2 
     if (cm && !(idx[u] & cm)) continue;
     if (KIND == KIND_GENERAL) {
       pair_update<KIND_GENERAL>(x0[u], x1[u], q);
-      ok0[u] = nonzero2(x0[u]);
     } else if (KIND == KIND_PHASE) {
       x1[u] = cmul(q[6], q[7], x1[u]);
-      suspect |= !(ok0[u] & nonzero2(x1[u]));
     } else {
       x0[u] = cmul(q[0], q[1], x0[u]);
       x1[u] = cmul(q[6], q[7], x1[u]);
-      ok0[u] = nonzero2(x0[u]);
-      suspect |= !(ok0[u] & nonzero2(x1[u]));
     }
   }
 }
@@ -629,25 +649,16 @@ __device__ __forceinline__ void stage_gate_fast(double2 (&x0)[SUNROLL], double2 
 template <int SIG>
 __device__ __forceinline__ bool stage_apply_fast(double2 (&x0)[SUNROLL], double2 (&x1)[SUNROLL],
                                                  const uint64_t (&idx)[SUNROLL], const StageParams &P) {
-  bool ok0[SUNROLL], suspect = false;
-#pragma unroll
-  for (int u = 0; u < SUNROLL; ++u) ok0[u] = nonzero2(x0[u]);
   int gi = 0;
   if (SIG == 1) {
     const StageGate &G = P.g[0];
     const uint64_t cm = G.cmask;
     if (G.kind == KIND_GENERAL)
-      stage_gate_fast<KIND_GENERAL>(x0, x1, ok0, idx, cm, G.q, suspect);
+      stage_gate_fast<KIND_GENERAL>(x0, x1, idx, cm, G.q);
     else if (G.kind == KIND_DIAG)
-      stage_gate_fast<KIND_DIAG>(x0, x1, ok0, idx, cm, G.q, suspect);
+      stage_gate_fast<KIND_DIAG>(x0, x1, idx, cm, G.q);
     else
-      stage_gate_fast<KIND_PHASE>(x0, x1, ok0, idx, cm, G.q, suspect);
-    // phases leave x0 alone on the fast path: test it once (conservatively, for
-    // every pair) instead of once per gate
-    bool all0 = true;
-#pragma unroll
-    for (int u = 0; u < SUNROLL; ++u) all0 &= ok0[u];
-    suspect |= !all0;
+      stage_gate_fast<KIND_PHASE>(x0, x1, idx, cm, G.q);
     // The pairs of a thread differ only in the index bits that separate the unrolled
     // rows; any other control bit has the same value for all of them, so one test
     // (on a 32-bit word when it can) decides the whole row set.
@@ -662,34 +673,31 @@ __device__ __forceinline__ bool stage_apply_fast(double2 (&x0)[SUNROLL], double2
       if (cm && !(cm & rows)) {
         if (!(idx[0] & cm)) continue;
 #pragma unroll
-        for (int u = 0; u < SUNROLL; ++u) {
-          x1[u] = cmul(qr, qi, x1[u]);
-          suspect |= (x1[u].x == 0.0) | (x1[u].y == 0.0);
-        }
+        for (int u = 0; u < SUNROLL; ++u) x1[u] = cmul(qr, qi, x1[u]);
         continue;
       }
 #pragma unroll
       for (int u = 0; u < SUNROLL; ++u) {
         if (cm && !(idx[u] & cm)) continue;
         x1[u] = cmul(qr, qi, x1[u]);
-        // zero test on the FP64 pipe (DSETP, predicate-accumulated): the ALU pipe is the
-        // busier one here.  x != 0.0 is false exactly for +-0 (NaN, subnormals count as nonzero).
-        suspect |= (x1[u].x == 0.0) | (x1[u].y == 0.0);
       }
     }
-    return suspect;
+  } else {
+    for (; gi < P.ngates; ++gi) {
+      const StageGate &G = P.g[gi];
+      const uint64_t cm = G.cmask;
+      if (G.kind == KIND_PHASE)
+        stage_gate_fast<KIND_PHASE>(x0, x1, idx, cm, G.q);
+      else if (G.kind == KIND_DIAG)
+        stage_gate_fast<KIND_DIAG>(x0, x1, idx, cm, G.q);
+      else
+        stage_gate_fast<KIND_GENERAL>(x0, x1, idx, cm, G.q);
+    }
   }
-  for (; gi < P.ngates; ++gi) {
-    const StageGate &G = P.g[gi];
-    const uint64_t cm = G.cmask;
-    if (G.kind == KIND_PHASE)
-      stage_gate_fast<KIND_PHASE>(x0, x1, ok0, idx, cm, G.q, suspect);
-    else if (G.kind == KIND_DIAG)
-      stage_gate_fast<KIND_DIAG>(x0, x1, ok0, idx, cm, G.q, suspect);
-    else
-      stage_gate_fast<KIND_GENERAL>(x0, x1, ok0, idx, cm, G.q, suspect);
-  }
-  return suspect;
+  bool ok = true;
+#pragma unroll
+  for (int u = 0; u < SUNROLL; ++u) ok &= nonzero2(x0[u]) & nonzero2(x1[u]);
+  return !ok;
 }
 
 // The exact path (replay): per-gate zero tests, falls back to mix() per pair.
@@ -730,6 +738,8 @@ __global__ void __launch_bounds__(BLK) k_stage_pairs(double2 *__restrict__ a, ui
     if (p < npairs) {
       x0[u] = a[i0[u]];
       x1[u] = a[i0[u] | tb];
+    } else {
+      x0[u] = x1[u] = make_double2(1.0, 1.0);  // tail rows: never trigger a replay
     }
   }
   if (__builtin_expect(stage_apply_fast<SIG>(x0, x1, i0, P), 0)) {
@@ -821,6 +831,8 @@ __global__ void __launch_bounds__(BLK) k_exchange_stage(double2 *__restrict__ mi
       const double2 am = mine[jj[u]], at = theirs[jj[u]];
       x0[u] = own_is_zero ? am : at;
       x1[u] = own_is_zero ? at : am;
+    } else {
+      x0[u] = x1[u] = make_double2(1.0, 1.0);
     }
   }
   if (__builtin_expect(stage_apply_fast<SIG>(x0, x1, jj, P), 0)) {
@@ -1088,6 +1100,7 @@ int launch_tile_t(double2 *a, int m, const TileParams &P, cudaStream_t st) {
   // speculation pays when diagonal/phase updates dominate the run (transform tails)
   return 2 * ndiag >= ngates ? launch_tile_ts<T, true>(a, m, P, st) : launch_tile_ts<T, false>(a, m, P, st);
 }
+
 
 int launch_tile(double2 *a, int m, int T, const TileParams &P, cudaStream_t st) {
   switch (T) {

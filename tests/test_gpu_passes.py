@@ -203,3 +203,30 @@ def test_speculative_paths_replay_exactly_on_zeros(n):
         sv.kernels.apply_gates(a, ops)
         torch.cuda.synchronize()
         assert bits_equal(a.cpu().numpy(), run_oracle(v, ops)), trial
+
+
+@pytest.mark.parametrize("n", [13, 16])
+def test_speculation_tests_only_the_final_values(n):
+    """The fused kernels test for zeros once, after the whole run (a dropped zero term of mix()
+    can only flip the sign of a zero).  Exact cancellations in the MIDDLE of a phase chain
+    -- (0.5+0.5j) * (0.5+0.5j) has real part exactly 0 -- must not change a bit whether the zero
+    survives to the end (replay) or is rotated away by the next phase (no replay)."""
+    rng = np.random.default_rng(77 + n)
+    cancel = sv.GateMatrix.unchecked([[1, 0], [0, 0.5 + 0.5j]])
+    rot = [sv.phase_r(3), sv.rotation_z(0.3), sv.pauli_z(), sv.GateMatrix.unchecked([[1, 0], [0, 1j]])]
+    v = np.full(1 << n, 0.5 + 0.5j, dtype=np.complex128)
+    for trial in range(3):
+        ops = []
+        for _ in range(60):
+            t = int(rng.integers(n if trial == 0 else (12 if trial == 1 else n - 1)))
+            if trial == 2:
+                t = n - 1  # one same-target stage
+            c = None if rng.random() < 0.4 else int((t + 1 + rng.integers(n - 1)) % n)
+            g = cancel if rng.random() < 0.4 else rot[int(rng.integers(len(rot)))]
+            ops.append(sv.GateOp(g, t, c))
+        if trial == 2:
+            ops.insert(0, sv.GateOp(sv.hadamard(), n - 1))
+        a = torch.from_numpy(v.copy()).to(DEV)
+        sv.kernels.apply_gates(a, ops)
+        torch.cuda.synchronize()
+        assert bits_equal(a.cpu().numpy(), run_oracle(v, ops)), trial
