@@ -20,13 +20,14 @@ SV_FUSED_MAX_TILE = 13
 SV_FUSED_MAX_GATES = 256
 SV_NORM_SCRATCH = 1025
 SV_STAGE_MAX_GATES = 64
+SV_MSTAGE_MAX_GATES, SV_MSTAGE_MAX_TARGETS = 128, 3
 SV_GROUP_GATES, SV_GROUP_TILE, SV_GROUP_STAGE = 0, 1, 2
 ABI_VERSION = 1
 
 EXPORTS = (
     "sv_version", "sv_last_error", "sv_launch_count", "sv_apply_single", "sv_apply_controlled",
     "sv_apply_fused", "sv_apply_gates", "sv_plan_gates", "sv_apply_group", "sv_exchange", "sv_exchange_chunk",
-    "sv_exchange_stage","sv_norm_sq", "sv_init_random", "sv_scale", "sv_init_basis",
+    "sv_exchange_stage", "sv_norm_sq", "sv_init_random", "sv_scale", "sv_init_basis",
     "sv_copy", "sv_ipc_handle", "sv_ipc_open", "sv_ipc_close",
 )
 

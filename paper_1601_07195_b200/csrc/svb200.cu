@@ -272,15 +272,6 @@ __device__ __forceinline__ void pair_update(double2 &a0, double2 &a1, const doub
   a1 = n1;
 }
 
-__device__ __forceinline__ void pair_update_kind(int kind, double2 &a0, double2 &a1, const double *q) {
-  if (kind == KIND_GENERAL)
-    pair_update<KIND_GENERAL>(a0, a1, q);
-  else if (kind == KIND_PHASE)
-    pair_update<KIND_PHASE>(a0, a1, q);
-  else
-    pair_update<KIND_DIAG>(a0, a1, q);
-}
-
 // ------------------------------------------------------- register-tiled fused runs
 //
 // One CTA per 2^T tile (T = 9..13), TR = 4 "register qubits": each of the
@@ -708,57 +699,246 @@ __device__ __forceinline__ void stage_apply_exact(double2 (&x0)[SUNROLL], double
   bool ok0[SUNROLL];
 #pragma unroll
   for (int u = 0; u < SUNROLL; ++u) ok0[u] = nonzero2(x0[u]);
-  int gi = 0;
   if (SIG == 1) {
     const StageGate &G = P.g[0];
     stage_gate_any(G.kind, x0, x1, ok0, idx, G.cmask, G.q);
-    for (gi = 1; gi < P.ngates; ++gi) {
+    for (int gi = 1; gi < P.ngates; ++gi) {
       const StageGate &H = P.g[gi];
       stage_gate<KIND_PHASE, SUNROLL>(x0, x1, ok0, idx, H.cmask, H.q);
     }
-    return;
-  }
-  for (; gi < P.ngates; ++gi) {
-    const StageGate &G = P.g[gi];
-    stage_gate_any(G.kind, x0, x1, ok0, idx, G.cmask, G.q);
+  } else {
+    for (int gi = 0; gi < P.ngates; ++gi) {
+      const StageGate &G = P.g[gi];
+      stage_gate_any(G.kind, x0, x1, ok0, idx, G.cmask, G.q);
+    }
   }
 }
 
-template <int SIG>
-__global__ void __launch_bounds__(BLK) k_stage_pairs(double2 *__restrict__ a, uint64_t npairs, int t,
-                                                     const StageParams P) {
-  const uint64_t tb = 1ull << t;
-  const uint64_t p0 = (uint64_t)blockIdx.x * (BLK * SUNROLL) + threadIdx.x;
-  double2 x0[SUNROLL], x1[SUNROLL];
-  uint64_t i0[SUNROLL];
+// ------------------------------------------------------------ multi-target stages
+//
+// A run of gates whose targets lie in at most MS_K = 3 slice bits ("slots"),
+// controls anywhere, in ONE HBM pass: each thread holds the 8 amplitudes that
+// span the three slot bits and applies the whole run in registers -- e.g. three
+// consecutive transform stages H(k), R(k, c) for all c < k.  A run with fewer
+// targets is padded with the most used control bits, which turns those
+// controls into compile-time pair patterns.
+//
+// A control on any other bit is decided per thread.  Above the bits that vary
+// across a warp it is warp-uniform, so the warp classifies 32 gates at a time
+// (one per lane) and ballots them into a mask of the gates that act anywhere in
+// the warp, then visits only those, in order: a gate whose control is clear
+// for the whole warp costs nothing.  Controls on lane bits stay per-lane (a
+// divergent skip).
+//
+// Updates: general complex gates run mix() (exact); "real" gates (every
+// imaginary part +-0) keep only the real products, Hadamard-like ones
+// (u00 = u01 = u10 = -u11, real) also share them between the two outputs
+// (8 FP64 ops per pair instead of 20); diagonal and phase gates only multiply.
+// Each differs from mix() at most in the sign of a zero, so one zero test of
+// the final eight amplitudes decides (see stage_gate_fast); a thread that sees
+// a zero replays its group exactly, out of line (ms_replay).
+
+#ifndef SV_MS_MINB
+#define SV_MS_MINB 4  // CTAs per SM the register budget must allow (measured: 2, 3, 4 -> QFT(30) 149, 120, 95 ms)
+#endif
+constexpr int MS_K = 3;
+constexpr int MS_N = 1 << MS_K;
+constexpr int MS_MAX = SV_MSTAGE_MAX_GATES;
+enum { MK_GENERAL = 0, MK_DIAG = 1, MK_PHASE = 2, MK_REAL = 3, MK_HSHARE = 4, MK_KINDS = 5 };
+
+struct MsGate {
+  int32_t code;  // (kind * MS_K + slot) * (MS_K + 1) + control slot (MS_K: none / not a slot)
+  int32_t pad;
+  double q[8];
+};
+
+// A run: consecutive gates with one code, inside one 32-gate ballot chunk h,
+// at chunk bits lo..hi.  The kernel dispatches once per run and loops over the
+// run's gates that act in the warp with the update compiled for that code.
+struct MsRun {
+  uint8_t code, h, lo, hi;
+};
+
+struct MsParams {
+  int32_t ngates;
+  int32_t nruns;
+  int32_t bits[MS_K];     // slice bit of each slot, ascending
+  int32_t pad;
+  uint8_t cbit[MS_MAX];   // control of gate g when it is not a slot bit, else 0xFF
+  MsRun run[MS_MAX + MS_MAX / 32];
+  MsGate g[MS_MAX];
+};
+
+template <int KIND>
+__device__ __forceinline__ void ms_pair(double2 &a0, double2 &a1, const double *q) {
+  if (KIND == MK_GENERAL) {
+    pair_update<KIND_GENERAL>(a0, a1, q);
+  } else if (KIND == MK_PHASE) {
+    a1 = cmul(q[6], q[7], a1);
+  } else if (KIND == MK_DIAG) {
+    a0 = cmul(q[0], q[1], a0);
+    a1 = cmul(q[6], q[7], a1);
+  } else if (KIND == MK_REAL) {
+    const double2 n0 = make_double2(__dadd_rn(__dmul_rn(q[0], a0.x), __dmul_rn(q[2], a1.x)),
+                                    __dadd_rn(__dmul_rn(q[0], a0.y), __dmul_rn(q[2], a1.y)));
+    a1 = make_double2(__dadd_rn(__dmul_rn(q[4], a0.x), __dmul_rn(q[6], a1.x)),
+                      __dadd_rn(__dmul_rn(q[4], a0.y), __dmul_rn(q[6], a1.y)));
+    a0 = n0;
+  } else {  // MK_HSHARE: round(-s * x) == -round(s * x)
+    const double s = q[0];
+    const double2 p0 = make_double2(__dmul_rn(s, a0.x), __dmul_rn(s, a0.y));
+    const double2 p1 = make_double2(__dmul_rn(s, a1.x), __dmul_rn(s, a1.y));
+    a0 = make_double2(__dadd_rn(p0.x, p1.x), __dadd_rn(p0.y, p1.y));
+    a1 = make_double2(__dsub_rn(p0.x, p1.x), __dsub_rn(p0.y, p1.y));
+  }
+}
+
+// gate on slot S, control slot C (MS_K: none), all pairs of the thread
+template <int S, int C, int KIND>
+__device__ __forceinline__ void ms_apply(double2 (&r)[MS_N], const double *qp) {
+  double q[8];
 #pragma unroll
-  for (int u = 0; u < SUNROLL; ++u) {
-    const uint64_t p = p0 + (uint64_t)u * BLK;
-    i0[u] = insert_zero(p, t);
-    if (p < npairs) {
-      x0[u] = a[i0[u]];
-      x1[u] = a[i0[u] | tb];
-    } else {
-      x0[u] = x1[u] = make_double2(1.0, 1.0);  // tail rows: never trigger a replay
+  for (int i = 0; i < 8; ++i) q[i] = qp[i];
+#pragma unroll
+  for (int j = 0; j < MS_N; ++j) {
+    if ((j >> S) & 1) continue;
+    if (C < MS_K && !((j >> C) & 1)) continue;
+    ms_pair<KIND>(r[j], r[j | (1 << S)], q);
+  }
+}
+
+// The gates of one run that act in this warp (act: chunk bits), in order; a
+// gate in lane_dep has its control on a lane bit and is skipped per lane.
+template <int S, int C, int KIND>
+__device__ __forceinline__ void ms_loop(double2 (&r)[MS_N], uint32_t act, uint32_t lane_dep, int g0, uint64_t base,
+                                        const MsParams &P) {
+  if (!lane_dep) {  // the common case: one path through the loop, no per-gate test
+    while (act) {
+      const int b = __ffs(act) - 1;
+      act &= act - 1;
+      ms_apply<S, C, KIND>(r, P.g[g0 + b].q);
     }
+    return;
   }
-  if (__builtin_expect(stage_apply_fast<SIG>(x0, x1, i0, P), 0)) {
+  while (act) {
+    const int b = __ffs(act) - 1;
+    act &= act - 1;
+    const int gi = g0 + b;
+    if (((lane_dep >> b) & 1u) && !((base >> P.cbit[gi]) & 1ull)) continue;
+    ms_apply<S, C, KIND>(r, P.g[gi].q);
+  }
+}
+
+__device__ __forceinline__ void ms_dispatch(int code, double2 (&r)[MS_N], uint32_t act, uint32_t lane_dep, int g0,
+                                            uint64_t base, const MsParams &P) {
+  switch (code) {
+#define MS_CASE(K_, S_, C_)                            \
+  case ((K_) * MS_K + (S_)) * (MS_K + 1) + (C_):      \
+    ms_loop<S_, C_, K_>(r, act, lane_dep, g0, base, P); \
+    break;
+#define MS_CASES_S(K_, S_) MS_CASE(K_, S_, 0) MS_CASE(K_, S_, 1) MS_CASE(K_, S_, 2) MS_CASE(K_, S_, 3)
+#define MS_CASES(K_) MS_CASES_S(K_, 0) MS_CASES_S(K_, 1) MS_CASES_S(K_, 2)
+    MS_CASES(MK_GENERAL) MS_CASES(MK_DIAG) MS_CASES(MK_PHASE) MS_CASES(MK_REAL) MS_CASES(MK_HSHARE)
+#undef MS_CASES
+#undef MS_CASES_S
+#undef MS_CASE
+    default: break;
+  }
+}
+
+__device__ __forceinline__ uint64_t ms_off(int j, uint64_t b0, uint64_t b1, uint64_t b2) {
+  return ((j & 1) ? b0 : 0ull) | ((j & 2) ? b1 : 0ull) | ((j & 4) ? b2 : 0ull);
+}
+
+// The speculative run (all 32 lanes of the warp take part).
+__device__ __forceinline__ void ms_run(double2 (&r)[MS_N], uint64_t base, const MsParams &P) {
+  const int lane = threadIdx.x & 31;
+  uint64_t vary = base ^ __shfl_sync(0xffffffffu, base, 0);  // index bits that differ between lanes
+  vary = ((uint64_t)__reduce_or_sync(0xffffffffu, (unsigned)(vary >> 32)) << 32) |
+         __reduce_or_sync(0xffffffffu, (unsigned)vary);
+  const uint64_t *cw = reinterpret_cast<const uint64_t *>(P.cbit);  // 8 control bytes per word
+  static_assert(MS_MAX == 128, "four ballot chunks");
+  uint32_t M0 = 0, M1 = 0, M2 = 0, M3 = 0, L0 = 0, L1 = 0, L2 = 0, L3 = 0;
 #pragma unroll
-    for (int u = 0; u < SUNROLL; ++u) {
-      if (p0 + (uint64_t)u * BLK < npairs) {
-        x0[u] = a[i0[u]];
-        x1[u] = a[i0[u] | tb];
-      }
-    }
-    stage_apply_exact<SIG>(x0, x1, i0, P);
+  for (int h = 0; h < 4; ++h) {
+    if (32 * h >= P.ngates) break;
+    const bool valid = 32 * h + lane < P.ngates;
+    // four uniform word loads and a select instead of 32 divergent constant loads
+    const uint64_t w0 = cw[4 * h], w1 = cw[4 * h + 1], w2 = cw[4 * h + 2], w3 = cw[4 * h + 3];
+    const int sel = lane >> 3;
+    const uint64_t w = sel == 0 ? w0 : sel == 1 ? w1 : sel == 2 ? w2 : w3;
+    const unsigned c = (unsigned)(w >> ((lane & 7) * 8)) & 0xFFu;
+    const bool mem = valid && c != 0xFFu;
+    const bool dep = mem && ((vary >> c) & 1ull);
+    const uint32_t mb = __ballot_sync(0xffffffffu, valid && (!mem || dep || ((base >> c) & 1ull)));
+    const uint32_t lb = __ballot_sync(0xffffffffu, dep);
+    if (h == 0) M0 = mb, L0 = lb;
+    if (h == 1) M1 = mb, L1 = lb;
+    if (h == 2) M2 = mb, L2 = lb;
+    if (h == 3) M3 = mb, L3 = lb;
+  }
+  for (int ri = 0; ri < P.nruns; ++ri) {
+    const MsRun R = P.run[ri];
+    const uint32_t range = (R.hi == 31 ? 0xffffffffu : ((2u << R.hi) - 1u)) & ~((1u << R.lo) - 1u);
+    const uint32_t mh = R.h == 0 ? M0 : R.h == 1 ? M1 : R.h == 2 ? M2 : M3;
+    const uint32_t lh = R.h == 0 ? L0 : R.h == 1 ? L1 : R.h == 2 ? L2 : L3;
+    const uint32_t act = mh & range;
+    if (act) ms_dispatch(R.code, r, act, lh & range, 32 * R.h, base, P);
+  }
+}
+
+template <int S>
+__device__ __forceinline__ void ms_exact(double2 (&r)[MS_N], int cs, const double *q) {
+#pragma unroll
+  for (int j = 0; j < MS_N; ++j) {
+    if ((j >> S) & 1) continue;
+    if (cs < MS_K && !((j >> cs) & 1)) continue;
+    pair_update<KIND_GENERAL>(r[j], r[j | (1 << S)], q);  // the definition itself
+  }
+}
+
+// Exact replay of one thread's group from global memory (nothing stored yet).
+__device__ __noinline__ void ms_replay(double2 *__restrict__ a, uint64_t base, const MsParams *P) {
+  const uint64_t b0 = 1ull << P->bits[0], b1 = 1ull << P->bits[1], b2 = 1ull << P->bits[2];
+  double2 r[MS_N];
+#pragma unroll
+  for (int j = 0; j < MS_N; ++j) r[j] = a[base | ms_off(j, b0, b1, b2)];
+  for (int gi = 0; gi < P->ngates; ++gi) {
+    const int c = P->cbit[gi];
+    if (c != 0xFF && !((base >> c) & 1ull)) continue;
+    const int code = P->g[gi].code;
+    const int cs = code % (MS_K + 1), s = (code / (MS_K + 1)) % MS_K;
+    if (s == 0)
+      ms_exact<0>(r, cs, P->g[gi].q);
+    else if (s == 1)
+      ms_exact<1>(r, cs, P->g[gi].q);
+    else
+      ms_exact<2>(r, cs, P->g[gi].q);
   }
 #pragma unroll
-  for (int u = 0; u < SUNROLL; ++u) {
-    const uint64_t p = p0 + (uint64_t)u * BLK;
-    if (p >= npairs) continue;
-    a[i0[u]] = x0[u];
-    a[i0[u] | tb] = x1[u];
+  for (int j = 0; j < MS_N; ++j) a[base | ms_off(j, b0, b1, b2)] = r[j];
+}
+
+__global__ void __launch_bounds__(BLK, SV_MS_MINB) k_mstage(double2 *__restrict__ a, uint64_t ngroups,
+                                                const __grid_constant__ MsParams P) {
+  const uint64_t p = (uint64_t)blockIdx.x * BLK + threadIdx.x;
+  const uint64_t b0 = 1ull << P.bits[0], b1 = 1ull << P.bits[1], b2 = 1ull << P.bits[2];
+  const uint64_t base = insert_zero(insert_zero(insert_zero(p, P.bits[0]), P.bits[1]), P.bits[2]);
+  const bool live = p < ngroups;
+  double2 r[MS_N];
+#pragma unroll
+  for (int j = 0; j < MS_N; ++j) r[j] = live ? a[base | ms_off(j, b0, b1, b2)] : make_double2(1.0, 1.0);
+  ms_run(r, base, P);
+  bool ok = true;
+#pragma unroll
+  for (int j = 0; j < MS_N; ++j) ok &= nonzero2(r[j]);
+  if (!live) return;
+  if (__builtin_expect(!ok, 0)) {
+    ms_replay(a, base, &P);
+    return;
   }
+#pragma unroll
+  for (int j = 0; j < MS_N; ++j) a[base | ms_off(j, b0, b1, b2)] = r[j];
 }
 
 // ---------------------------------------------------------------- half exchange
@@ -1141,34 +1321,90 @@ int stage_sig(const StageParams &P) {
   return 1;
 }
 
-int run_stage(double2 *a, int m, const sv_gate *gates, int n, cudaStream_t st) {
-  static thread_local StageParams P;
-  const int t = gates[0].target;
-  P.ngates = n;
-  for (int i = 0; i < n; ++i) {
-    P.g[i].cmask = gates[i].control >= 0 ? (1ull << gates[i].control) : 0ull;
-    P.g[i].kind = classify_kind(gates[i].q);
-    memcpy(P.g[i].q, gates[i].q, sizeof(P.g[i].q));
+int ms_kind(const double *q) {
+  const bool z12 = q[2] == 0.0 && q[3] == 0.0, z21 = q[4] == 0.0 && q[5] == 0.0;
+  if (z12 && z21) return (q[0] == 1.0 && q[1] == 0.0) ? MK_PHASE : MK_DIAG;
+  if (!(q[1] == 0.0 && q[3] == 0.0 && q[5] == 0.0 && q[7] == 0.0)) return MK_GENERAL;
+  return (q[0] == q[2] && q[0] == q[4] && q[0] == -q[6]) ? MK_HSHARE : MK_REAL;
+}
+
+// One multi-target stage launch: gates[0..n) with targets in <= MS_K bits.
+int run_mstage(double2 *a, int m, const sv_gate *gates, int n, cudaStream_t st) {
+  static thread_local MsParams P;
+  if (n < 1 || n > MS_MAX) return fail(SV_EINVAL, "stage group: %d gates not in [1, %d]", n, MS_MAX);
+  if (m < MS_K) return fail(SV_EINVAL, "stage group: m=%d below %d", m, MS_K);
+  int bits[MS_K], nb = 0;
+  for (int k = 0; k < n; ++k) {
+    const int t = gates[k].target;
+    bool in = false;
+    for (int s = 0; s < nb; ++s) in |= bits[s] == t;
+    if (in) continue;
+    if (nb == MS_K) return fail(SV_EINVAL, "stage group: more than %d distinct targets", MS_K);
+    bits[nb++] = t;
   }
-  const uint64_t np = 1ull << (m - 1);
-  if (stage_sig(P) == 1)
-    k_stage_pairs<1><<<grid_for(np, BLK * SUNROLL), BLK, 0, st>>>(a, np, t, P);
-  else
-    k_stage_pairs<0><<<grid_for(np, BLK * SUNROLL), BLK, 0, st>>>(a, np, t, P);
-  return after_launch("k_stage_pairs");
+  // pad with the most used other controls (their gates become pair patterns), then high bits
+  int uses[64] = {0};
+  for (int k = 0; k < n; ++k)
+    if (gates[k].control >= 0) ++uses[gates[k].control];
+  while (nb < MS_K) {
+    int best = -1;
+    for (int b = m - 1; b >= 0; --b) {
+      bool in = false;
+      for (int s = 0; s < nb; ++s) in |= bits[s] == b;
+      if (!in && (best < 0 || uses[b] > uses[best])) best = b;
+    }
+    bits[nb++] = best;
+  }
+  std::sort(bits, bits + MS_K);
+  P.ngates = n;
+  for (int s = 0; s < MS_K; ++s) P.bits[s] = bits[s];
+  memset(P.cbit, 0xFF, sizeof(P.cbit));
+  auto slot = [&](int b) {
+    for (int s = 0; s < MS_K; ++s)
+      if (bits[s] == b) return s;
+    return MS_K;
+  };
+  for (int k = 0; k < n; ++k) {
+    const int c = gates[k].control, cs = c >= 0 ? slot(c) : MS_K;
+    if (c >= 0 && cs == MS_K) P.cbit[k] = (uint8_t)c;
+    P.g[k].code = (ms_kind(gates[k].q) * MS_K + slot(gates[k].target)) * (MS_K + 1) + cs;
+    P.g[k].pad = 0;
+    memcpy(P.g[k].q, gates[k].q, sizeof(P.g[k].q));
+  }
+  P.nruns = 0;
+  for (int k = 0; k < n; ++k) {
+    MsRun &R = P.run[P.nruns];
+    const bool extend = k > 0 && R.code == P.g[k].code && R.h == k / 32;
+    if (!extend) {
+      MsRun &N = P.run[k > 0 ? ++P.nruns : P.nruns];
+      N.code = (uint8_t)P.g[k].code;
+      N.h = (uint8_t)(k / 32);
+      N.lo = (uint8_t)(k % 32);
+    }
+    P.run[P.nruns].hi = (uint8_t)(k % 32);
+  }
+  ++P.nruns;
+  const uint64_t ng = 1ull << (m - MS_K);
+  k_mstage<<<grid_for(ng, BLK), BLK, 0, st>>>(a, ng, P);
+  return after_launch("k_mstage");
 }
 
 // Native pass planner: the launch group starting at gates[i], returned as its end.
 // Candidate 1, a register-tiled run: targets below L = T-4, or one of up to four
 // higher slice bits taken in order of appearance (the tile then gathers those
-// bits).  Candidate 2, a same-target stage.  Cost model (B200, ms at 2^30
-// amplitudes, compute overlapping HBM): a pass costs max(5, sum of per-gate
-// costs), per gate tile 1.15 general / 0.45 diagonal, stage 0.6 / 0.37.  The
-// stage is taken when it plus a tile over the rest of the candidate run costs
-// less than the candidate run as one tile.  A lone gate is a single-gate launch.
-// Pure host code (sv_plan_gates exposes it).
+// bits).  Candidate 2, a stage: the run whose targets stay within MS_K = 3
+// distinct bits.  Cost model (B200, ms at 2^30 amplitudes, compute overlapping
+// HBM): a pass costs max(5, sum of per-gate costs); per gate, tile 1.15
+// general / 0.45 diagonal, stage by structure (general 0.9, real 0.55,
+// Hadamard-like 0.35, diagonal 0.35, phase 0.18; half that when controlled).
+// The candidate with the lower cost per gate wins (ties: the stage).  A lone
+// gate is a single-gate launch.  Pure host code (sv_plan_gates exposes it).
+double stage_cost(const sv_gate &g) {
+  static const double c[MK_KINDS] = {0.9, 0.35, 0.18, 0.55, 0.35};
+  return c[ms_kind(g.q)] * (g.control >= 0 ? 0.5 : 1.0);
+}
+
 int next_group(int m, const sv_gate *gates, int n, int i, int T, int *kind) {
-  (void)m;
   const int L = T - TR;
   auto tile_cost = [&](int k) { return classify_kind(gates[k].q) == KIND_GENERAL ? 1.15 : 0.45; };
   auto pass = [](double c) { return c > 5.0 ? c : 5.0; };
@@ -1186,45 +1422,37 @@ int next_group(int m, const sv_gate *gates, int n, int i, int T, int *kind) {
       ct += tile_cost(ja);
     }
   }
-  const int t0 = gates[i].target;
-  int jb = i + 1;
-  double cs = classify_kind(gates[i].q) == KIND_GENERAL ? 0.6 : 0.37, ctb = tile_cost(i);
-  while (jb < n && gates[jb].target == t0 && jb - i < STAGE_MAX_GATES) {
-    cs += classify_kind(gates[jb].q) == KIND_GENERAL ? 0.6 : 0.37;
-    ctb += tile_cost(jb);
-    ++jb;
+  int S[MS_K], ns = 0, jb = i;
+  double cs = 0.0;
+  if (m >= MS_K + 5) {
+    for (; jb < n && jb - i < MS_MAX; ++jb) {
+      const int tt = gates[jb].target;
+      bool in = false;
+      for (int k = 0; k < ns && !in; ++k) in = S[k] == tt;
+      if (!in) {
+        if (ns == MS_K) break;
+        S[ns++] = tt;
+      }
+      cs += stage_cost(gates[jb]);
+    }
   }
   const int A = ja - i, B = jb - i;
-  const bool stage_better = B >= A ? pass(cs) <= pass(ct) : pass(cs) + pass(ct - ctb) < pass(ct);
   if (A <= 1 && B <= 1) {
     *kind = SV_GROUP_GATES;
     return i + 1;
   }
-  if (t0 >= 5 && B > 1 && stage_better) {
+  if (B > 1 && (A <= 1 || pass(cs) / B <= pass(ct) / A)) {
     *kind = SV_GROUP_STAGE;
     return jb;
   }
-  if (A > 1) {
-    *kind = SV_GROUP_TILE;
-    return ja;
-  }
-  *kind = SV_GROUP_GATES;
-  return jb;
+  *kind = SV_GROUP_TILE;
+  return ja;
 }
 
 int exec_group(double2 *a, int m, int T, int kind, const sv_gate *gates, int n, cudaStream_t st) {
   if (kind == SV_GROUP_STAGE) {
-    for (int k = 1; k < n; ++k)
-      if (gates[k].target != gates[0].target) return fail(SV_EINVAL, "stage group: targets differ");
-    if (n > STAGE_MAX_GATES) return fail(SV_EINVAL, "stage group: more than %d gates", STAGE_MAX_GATES);
-    if (n == 1 || gates[0].target < 5) {
-      for (int k = 0; k < n; ++k) {
-        const int rc = launch_gate(a, m, gates[k], st);
-        if (rc != SV_OK) return rc;
-      }
-      return SV_OK;
-    }
-    return run_stage(a, m, gates, n, st);
+    if (n == 1) return launch_gate(a, m, gates[0], st);
+    return run_mstage(a, m, gates, n, st);
   }
   if (kind == SV_GROUP_TILE && T >= 9 && n > 1) {
     const int L = T - TR;

@@ -1,0 +1,110 @@
+"""GPU: multi-target stage passes (k_mstage) -- bitwise against the oracle.
+
+One stage launch applies a run of gates whose targets lie in at most three
+qubits; controls anywhere: on a slot bit (compile-time pair pattern), on a lane
+bit (per-lane), above the lanes (warp-uniform ballot), including runs longer
+than 32 gates (several ballot chunks) and the 128-gate maximum.  Every update
+shape (general, real, Hadamard-like, diagonal, phase) is in the zoo, and
+zero-salted states force the exact replay.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import random_state
+from test_gpu_passes import DEV, bits_equal, gate_zoo, run_oracle, with_zeros
+
+pytestmark = pytest.mark.gpu
+
+sv = pytest.importorskip("paper_1601_07195_b200")
+from paper_1601_07195_b200 import _lib  # noqa: E402
+from paper_1601_07195_b200.kernels import device_view, gate_array, stream_handle  # noqa: E402
+
+
+def apply_stage(a, ops):
+    ptr, m = device_view(a)
+    rc = _lib.load().sv_apply_group(ptr, m, _lib.SV_GROUP_STAGE, gate_array(ops), len(ops), 0, stream_handle())
+    _lib.check(rc)
+
+
+def stage_ops(rng, n, targets, count, cfrac=0.7, controls=None):
+    zoo = gate_zoo(rng) + [sv.GateMatrix.unchecked([[0.5, -0.25], [0.75, 1.5]]),  # real, not unitary
+                           sv.GateMatrix.unchecked([[0.25, 0.25], [0.25, -0.25]])]  # Hadamard-like
+    ops = []
+    for _ in range(count):
+        t = int(targets[int(rng.integers(len(targets)))])
+        c = None
+        if rng.random() < cfrac:
+            pool = controls if controls is not None else range(n)
+            cands = [x for x in pool if x != t]
+            c = int(cands[int(rng.integers(len(cands)))])
+        ops.append(sv.GateOp(zoo[int(rng.integers(len(zoo)))], t, c))
+    return ops
+
+
+@pytest.mark.parametrize("n,targets", [(8, [5, 6, 7]), (12, [11, 3, 7]), (14, [0, 1, 2]), (16, [9]),
+                                       (16, [15, 4]), (18, [17, 16, 15]), (20, [8, 0, 19])])
+def test_stage_runs_bitwise(n, targets):
+    rng = np.random.default_rng(4000 + 31 * n + sum(targets))
+    for trial in range(3):
+        v = with_zeros(rng, n) if trial == 2 else random_state(rng, n)
+        ops = stage_ops(rng, n, targets, [20, 77, 128][trial])
+        a = torch.from_numpy(v.copy()).to(DEV)
+        apply_stage(a, ops)
+        torch.cuda.synchronize()
+        assert bits_equal(a.cpu().numpy(), run_oracle(v, ops)), (n, targets, trial)
+
+
+@pytest.mark.parametrize("ctl", ["lanes", "warp", "cta", "slots"])
+def test_stage_control_placements(ctl):
+    """Controls only on lane bits (0..4), warp bits (5..7), CTA bits (>= 11) or the slot bits."""
+    n, targets = 17, [8, 9, 10]
+    pool = {"lanes": range(5), "warp": range(5, 8), "cta": range(11, n), "slots": targets}[ctl]
+    rng = np.random.default_rng({"lanes": 1, "warp": 2, "cta": 3, "slots": 4}[ctl])
+    v = random_state(rng, n)
+    ops = stage_ops(rng, n, targets, 100, cfrac=0.9, controls=list(pool))
+    a = torch.from_numpy(v.copy()).to(DEV)
+    apply_stage(a, ops)
+    torch.cuda.synchronize()
+    assert bits_equal(a.cpu().numpy(), run_oracle(v, ops)), ctl
+
+
+def test_stage_replay_on_zero_results():
+    """Basis states (mostly exact zeros) and mid-chain cancellations take the exact replay."""
+    n = 15
+    rng = np.random.default_rng(7)
+    for v in (np.eye(1, 1 << n, 1234, dtype=np.complex128)[0], np.full(1 << n, 0.5 + 0.5j)):
+        ops = [sv.GateOp(sv.hadamard(), 14)]
+        ops += [sv.GateOp(sv.GateMatrix.unchecked([[1, 0], [0, 0.5 + 0.5j]]), t, c)
+                for t, c in zip([14, 13, 12] * 10, rng.integers(0, 12, 30))]
+        ops += stage_ops(rng, n, [12, 13, 14], 40)
+        a = torch.from_numpy(v.copy()).to(DEV)
+        apply_stage(a, ops)
+        torch.cuda.synchronize()
+        assert bits_equal(a.cpu().numpy(), run_oracle(v, ops))
+
+
+def test_qft_plan_runs_through_stages_bitwise():
+    n = 21
+    rng = np.random.default_rng(21)
+    v = with_zeros(rng, n, frac=0.05)
+    circ = sv.build_qft(n)
+    st = sv.LocalState(sv.Layout(n), torch.from_numpy(v.copy()).to(DEV))
+    sv.run_circuit(st, circ, fusion=sv.FusionConfig(l_c=12, passes=True))
+    torch.cuda.synchronize()
+    assert bits_equal(st.amps.cpu().numpy(), run_oracle(v, circ.gates))
+
+
+def test_stage_abi_guards():
+    a = torch.zeros(1 << 10, dtype=torch.complex128, device=DEV)
+    ptr, m = device_view(a)
+    L = _lib.load()
+    four = [sv.GateOp(sv.hadamard(), t) for t in (1, 2, 3, 4)]
+    assert L.sv_apply_group(ptr, m, _lib.SV_GROUP_STAGE, gate_array(four), 4, 0, stream_handle()) == _lib.SV_EINVAL
+    assert "distinct targets" in L.sv_last_error().decode()
+    many = [sv.GateOp(sv.hadamard(), 1)] * (_lib.SV_MSTAGE_MAX_GATES + 1)
+    assert L.sv_apply_group(ptr, m, _lib.SV_GROUP_STAGE, gate_array(many), len(many), 0,
+                            stream_handle()) == _lib.SV_EINVAL

@@ -8,16 +8,15 @@ import paper_1601_07195_b200 as sv
 from paper_1601_07195_b200.passes import _resolve_rank_controls, tile_for
 
 
-def test_qft_plan_is_one_pass_per_high_stage():
+def test_qft_plan_is_one_pass_per_three_stages():
     n, m = 30, 30
     circ = sv.build_qft(n)
     plan = sv.plan_passes(circ.gates, m, 12)
-    kinds = [p.kind for p in plan]
-    # every high transform stage is one same-target pass, the low stages one register-tiled run
-    k = kinds.index("local_tile")
-    assert kinds[:k] == ["local_stage"] * k and kinds[k:] == ["local_tile"] and 18 <= k <= 24
-    assert [p.target for p in plan[:k]] == list(range(29, 29 - k, -1))
+    # three consecutive transform stages H(k), R(k, c) for all c < k share one stage pass
+    assert [p.kind for p in plan] == ["local_stage"] * 10
+    assert [sorted({op.target for op in p.gates}) for p in plan] == [[k - 2, k - 1, k] for k in range(29, 0, -3)]
     assert [op for p in plan for op in p.gates] == list(circ.gates)
+    assert max(len(p.gates) for p in plan) <= sv._lib.SV_MSTAGE_MAX_GATES
 
 
 def test_random_circuit_plan_fuses_high_targets():
@@ -31,7 +30,7 @@ def test_random_circuit_plan_fuses_high_targets():
             high = {op.target for op in p.gates if op.target >= 8}
             assert len(high) <= 4
         if p.kind == "local_stage":
-            assert len({op.target for op in p.gates}) == 1
+            assert len({op.target for op in p.gates}) <= sv._lib.SV_MSTAGE_MAX_TARGETS
 
 
 def test_global_stages_and_order_preserved():
@@ -55,7 +54,7 @@ def test_plan_is_rank_independent_and_tile_bounds():
             if p.kind == "local_tile":  # low bits < T-4 plus at most four gathered high bits
                 assert len({op.target for op in p.gates if op.target >= tile_for(12, m) - 4}) <= 4
             if p.kind == "local_stage":
-                assert len({op.target for op in p.gates}) == 1 and p.target >= 5
+                assert len({op.target for op in p.gates}) <= 3 and len(p.gates) > 1
     assert tile_for(5, 30) == 0 and tile_for(20, 30) == 13 and tile_for(12, 11) == 11
 
 
@@ -67,7 +66,7 @@ from hypothesis import strategies as st  # noqa: E402
 @settings(max_examples=60, deadline=None)
 def test_native_planner_invariants(m, seed, tile):
     """sv_plan_gates (the planner sv_apply_gates runs): order-preserving cover, one launch per
-    group, tile groups gather at most four bits above T-4, stages share one target >= 5."""
+    group, tile groups gather at most four bits above T-4, stages span at most three targets."""
     rng = np.random.default_rng(seed)
     T = tile if tile and tile <= min(m, 13) else min(m, 13)
     zoo = [sv.hadamard(), sv.phase_r(3), sv.pauli_z(), sv.random_unitary(rng)]
@@ -84,7 +83,7 @@ def test_native_planner_invariants(m, seed, tile):
             assert len(p.gates) <= sv._lib.SV_FUSED_MAX_GATES
             assert len({t for t in targets if t >= T - 4}) <= 4
         elif p.kind == "local_stage":
-            assert len(targets) == 1 and p.target >= 5 and len(p.gates) <= sv._lib.SV_STAGE_MAX_GATES
+            assert len(targets) <= sv._lib.SV_MSTAGE_MAX_TARGETS and 1 < len(p.gates) <= sv._lib.SV_MSTAGE_MAX_GATES
         else:
             assert p.kind == "local_gate"
 
