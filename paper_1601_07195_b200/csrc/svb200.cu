@@ -59,7 +59,8 @@ GateQ load_q(const double *q) {
 // ------------------------------------------------------------------ arithmetic
 
 __device__ __forceinline__ double2 cmul(double rr, double ri, double2 a) {
-  return make_double2(__fma_rn(rr, a.x, -__dmul_rn(a.y, ri)), __fma_rn(rr, a.y, __dmul_rn(a.x, ri)));
+  const double t_im = __dmul_rn(a.y, ri), t_re = __dmul_rn(a.x, ri);  // both products first
+  return make_double2(__fma_rn(rr, a.x, -t_im), __fma_rn(rr, a.y, t_re));
 }
 
 __device__ __forceinline__ double2 mix(double2 a0, double2 a1, double r0r, double r0i, double r1r,
