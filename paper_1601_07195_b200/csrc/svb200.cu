@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(FusedShape<T>::NT) k_fused(double2 *__restrict
 //                 cmul(1,a0) == a0 whenever a0 has no zero component, so new0 is a0 untouched.
 // Zero tests are integer tests on the bit patterns (ALU pipe, not FP64).
 
-enum { KIND_GENERAL = 0, KIND_DIAG = 1, KIND_PHASE = 2 };
+enum { KIND_GENERAL = 0, KIND_DIAG = 1, KIND_PHASE = 2, KIND_REAL = 3, KIND_HSHARE = 4, KIND_COUNT = 5 };
 
 __device__ __forceinline__ bool nonzero2(double2 v) {
   const int mx = (__double2hiint(v.x) & 0x7fffffff) | __double2loint(v.x);
@@ -271,6 +271,37 @@ __device__ __forceinline__ void pair_update(double2 &a0, double2 &a1, const doub
   }
   a0 = n0;
   a1 = n1;
+}
+
+// Speculative pair updates (the fused kernels test their final values for
+// zeros and replay exactly if they see one -- see stage_gate_fast):
+//   KIND_PHASE / KIND_DIAG  products only;
+//   KIND_REAL    every imaginary part +-0: real products only, round(u.re * a) per component;
+//   KIND_HSHARE  real with u00 = u01 = u10 = -u11 = s (Hadamard-like): the products s*a0, s*a1 are
+//                shared by both outputs (round(-s*x) == -round(s*x)): 8 FP64 ops instead of 20.
+// Each equals mix() up to the signs of zeros.
+template <int KIND>
+__device__ __forceinline__ void spec_pair(double2 &a0, double2 &a1, const double *q) {
+  if (KIND == KIND_GENERAL) {
+    pair_update<KIND_GENERAL>(a0, a1, q);
+  } else if (KIND == KIND_PHASE) {
+    a1 = cmul(q[6], q[7], a1);
+  } else if (KIND == KIND_DIAG) {
+    a0 = cmul(q[0], q[1], a0);
+    a1 = cmul(q[6], q[7], a1);
+  } else if (KIND == KIND_REAL) {
+    const double2 n0 = make_double2(__dadd_rn(__dmul_rn(q[0], a0.x), __dmul_rn(q[2], a1.x)),
+                                    __dadd_rn(__dmul_rn(q[0], a0.y), __dmul_rn(q[2], a1.y)));
+    a1 = make_double2(__dadd_rn(__dmul_rn(q[4], a0.x), __dmul_rn(q[6], a1.x)),
+                      __dadd_rn(__dmul_rn(q[4], a0.y), __dmul_rn(q[6], a1.y)));
+    a0 = n0;
+  } else {  // KIND_HSHARE
+    const double s = q[0];
+    const double2 p0 = make_double2(__dmul_rn(s, a0.x), __dmul_rn(s, a0.y));
+    const double2 p1 = make_double2(__dmul_rn(s, a1.x), __dmul_rn(s, a1.y));
+    a0 = make_double2(__dadd_rn(p0.x, p1.x), __dadd_rn(p0.y, p1.y));
+    a1 = make_double2(__dsub_rn(p0.x, p1.x), __dsub_rn(p0.y, p1.y));
+  }
 }
 
 // ------------------------------------------------------- register-tiled fused runs
@@ -357,25 +388,24 @@ constexpr int TG = 2;
 // with their products only; k_tile tests the final tile once and replays it
 // from global memory with spec = false if any component is zero (see
 // stage_gate_fast for why that one test is enough).
-template <int TB, int KIND, bool FULL>
-__device__ __forceinline__ void tile_gate_k(double2 (&r)[TRN], uint32_t pm, const double *qp, bool spec) {
+template <int TB, int KIND, bool FULL, bool SPEC>
+__device__ __forceinline__ void tile_gate_k(double2 (&r)[TRN], uint32_t pm, const double *qp) {
   double q[8];  // once per gate in registers, not one constant-bank load per pair
 #pragma unroll
   for (int i = 0; i < 8; ++i) q[i] = qp[i];
 #define PAIRS(k) ((((k) >> TB) << (TB + 1)) | ((k) & ((1 << TB) - 1)))  // k-th j with bit TB clear
-  if (KIND != KIND_GENERAL && spec) {
+  if (KIND != KIND_GENERAL && SPEC) {
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const int j = PAIRS(k);
       if (!(FULL || ((pm >> j) & 1u))) continue;
-      if (KIND == KIND_DIAG) r[j] = cmul(q[0], q[1], r[j]);
-      r[j | (1 << TB)] = cmul(q[6], q[7], r[j | (1 << TB)]);
+      spec_pair<KIND>(r[j], r[j | (1 << TB)], q);
     }
     return;
   }
 #pragma unroll
   for (int grp = 0; grp < 8 / TG; ++grp) {
-    if (KIND == KIND_GENERAL) {
+    if (KIND == KIND_GENERAL || KIND >= KIND_REAL) {  // exact pass: real kinds run mix()
 #pragma unroll
       for (int k = 0; k < TG; ++k) {
         const int j = PAIRS(grp * TG + k);
@@ -412,31 +442,34 @@ __device__ __forceinline__ void tile_gate_k(double2 (&r)[TRN], uint32_t pm, cons
   }
 }
 
-template <int TB>
-__device__ __forceinline__ void tile_gate(double2 (&r)[TRN], uint32_t pm, int kind, const double *q, bool spec) {
+template <int TB, bool SPEC>
+__device__ __forceinline__ void tile_gate(double2 (&r)[TRN], uint32_t pm, int kind, const double *q) {
   if (pm == 0u) return;
+  if (!SPEC && kind >= KIND_REAL) kind = KIND_GENERAL;  // the exact pass runs mix() for them
   if (pm == 0xFFFFu) {  // uncontrolled, or control decided per thread/CTA: straight-line code
-    if (kind == KIND_GENERAL)
-      tile_gate_k<TB, KIND_GENERAL, true>(r, pm, q, spec);
-    else if (kind == KIND_PHASE)
-      tile_gate_k<TB, KIND_PHASE, true>(r, pm, q, spec);
-    else
-      tile_gate_k<TB, KIND_DIAG, true>(r, pm, q, spec);
+    switch (kind) {
+      case KIND_GENERAL: tile_gate_k<TB, KIND_GENERAL, true, SPEC>(r, pm, q); break;
+      case KIND_PHASE: tile_gate_k<TB, KIND_PHASE, true, SPEC>(r, pm, q); break;
+      case KIND_DIAG: tile_gate_k<TB, KIND_DIAG, true, SPEC>(r, pm, q); break;
+      case KIND_REAL: if (SPEC) tile_gate_k<TB, KIND_REAL, true, SPEC>(r, pm, q); break;
+      default: if (SPEC) tile_gate_k<TB, KIND_HSHARE, true, SPEC>(r, pm, q); break;
+    }
     return;
   }
-  if (kind == KIND_GENERAL)
-    tile_gate_k<TB, KIND_GENERAL, false>(r, pm, q, spec);
-  else if (kind == KIND_PHASE)
-    tile_gate_k<TB, KIND_PHASE, false>(r, pm, q, spec);
-  else
-    tile_gate_k<TB, KIND_DIAG, false>(r, pm, q, spec);
+  switch (kind) {
+    case KIND_GENERAL: tile_gate_k<TB, KIND_GENERAL, false, SPEC>(r, pm, q); break;
+    case KIND_PHASE: tile_gate_k<TB, KIND_PHASE, false, SPEC>(r, pm, q); break;
+    case KIND_DIAG: tile_gate_k<TB, KIND_DIAG, false, SPEC>(r, pm, q); break;
+    case KIND_REAL: if (SPEC) tile_gate_k<TB, KIND_REAL, false, SPEC>(r, pm, q); break;
+    default: if (SPEC) tile_gate_k<TB, KIND_HSHARE, false, SPEC>(r, pm, q); break;
+  }
 }
 
 // One tile through the run: load (natural layout), segments with transposes,
 // back to the natural layout in registers (the caller stores).
-template <int T>
+template <int T, bool SPEC>
 __device__ __forceinline__ void tile_body(const double2 *__restrict__ a, uint64_t tile0, const int (&hb)[TR],
-                                          int tid, const TileParams &P, double2 *s, double2 (&r)[TRN], bool spec) {
+                                          int tid, const TileParams &P, double2 *s, double2 (&r)[TRN]) {
   constexpr int NT = 1 << (T - TR);
 #pragma unroll
   for (int j = 0; j < TRN; ++j) r[j] = a[tile0 + tile_off<T>(tid, j, hb)];
@@ -470,10 +503,10 @@ __device__ __forceinline__ void tile_body(const double2 *__restrict__ a, uint64_
       else if (G.cmode == 3)
         pm = ((tile0 >> G.cabove) & 1ull) ? 0xFFFFu : 0u;
       switch (G.tb) {
-        case 0: tile_gate<0>(r, pm, G.kind, G.q, spec); break;
-        case 1: tile_gate<1>(r, pm, G.kind, G.q, spec); break;
-        case 2: tile_gate<2>(r, pm, G.kind, G.q, spec); break;
-        default: tile_gate<3>(r, pm, G.kind, G.q, spec); break;
+        case 0: tile_gate<0, SPEC>(r, pm, G.kind, G.q); break;
+        case 1: tile_gate<1, SPEC>(r, pm, G.kind, G.q); break;
+        case 2: tile_gate<2, SPEC>(r, pm, G.kind, G.q); break;
+        default: tile_gate<3, SPEC>(r, pm, G.kind, G.q); break;
       }
     }
   }
@@ -497,7 +530,7 @@ __device__ __noinline__ void tile_replay(double2 *__restrict__ a, uint64_t tile0
   const int hb[TR] = {hb0, hb1, hb2, hb3};
   const int tid = threadIdx.x;
   double2 r[TRN];
-  tile_body<T>(a, tile0, hb, tid, *P, s, r, false);
+  tile_body<T, false>(a, tile0, hb, tid, *P, s, r);
 #pragma unroll
   for (int j = 0; j < TRN; ++j) a[tile0 + tile_off<T>(tid, j, hb)] = r[j];
 }
@@ -516,7 +549,7 @@ __global__ void __launch_bounds__(1 << (T - TR), (T <= 12) ? 2 : 1)
   const uint64_t tile0 = tile_base<T>(blockIdx.x, hb);  // every non-tile slice bit of this CTA
   const int tid = threadIdx.x;
   double2 r[TRN];
-  tile_body<T>(a, tile0, hb, tid, P, s, r, SPEC);
+  tile_body<T, SPEC>(a, tile0, hb, tid, P, s, r);
   if (SPEC) {
     bool ok = true;
 #pragma unroll
@@ -745,7 +778,6 @@ __device__ __forceinline__ void stage_apply_exact(double2 (&x0)[SUNROLL], double
 constexpr int MS_K = 3;
 constexpr int MS_N = 1 << MS_K;
 constexpr int MS_MAX = SV_MSTAGE_MAX_GATES;
-enum { MK_GENERAL = 0, MK_DIAG = 1, MK_PHASE = 2, MK_REAL = 3, MK_HSHARE = 4, MK_KINDS = 5 };
 
 struct MsGate {
   int32_t code;  // (kind * MS_K + slot) * (MS_K + 1) + control slot (MS_K: none / not a slot)
@@ -770,30 +802,6 @@ struct MsParams {
   MsGate g[MS_MAX];
 };
 
-template <int KIND>
-__device__ __forceinline__ void ms_pair(double2 &a0, double2 &a1, const double *q) {
-  if (KIND == MK_GENERAL) {
-    pair_update<KIND_GENERAL>(a0, a1, q);
-  } else if (KIND == MK_PHASE) {
-    a1 = cmul(q[6], q[7], a1);
-  } else if (KIND == MK_DIAG) {
-    a0 = cmul(q[0], q[1], a0);
-    a1 = cmul(q[6], q[7], a1);
-  } else if (KIND == MK_REAL) {
-    const double2 n0 = make_double2(__dadd_rn(__dmul_rn(q[0], a0.x), __dmul_rn(q[2], a1.x)),
-                                    __dadd_rn(__dmul_rn(q[0], a0.y), __dmul_rn(q[2], a1.y)));
-    a1 = make_double2(__dadd_rn(__dmul_rn(q[4], a0.x), __dmul_rn(q[6], a1.x)),
-                      __dadd_rn(__dmul_rn(q[4], a0.y), __dmul_rn(q[6], a1.y)));
-    a0 = n0;
-  } else {  // MK_HSHARE: round(-s * x) == -round(s * x)
-    const double s = q[0];
-    const double2 p0 = make_double2(__dmul_rn(s, a0.x), __dmul_rn(s, a0.y));
-    const double2 p1 = make_double2(__dmul_rn(s, a1.x), __dmul_rn(s, a1.y));
-    a0 = make_double2(__dadd_rn(p0.x, p1.x), __dadd_rn(p0.y, p1.y));
-    a1 = make_double2(__dsub_rn(p0.x, p1.x), __dsub_rn(p0.y, p1.y));
-  }
-}
-
 // gate on slot S, control slot C (MS_K: none), all pairs of the thread
 template <int S, int C, int KIND>
 __device__ __forceinline__ void ms_apply(double2 (&r)[MS_N], const double *qp) {
@@ -804,7 +812,7 @@ __device__ __forceinline__ void ms_apply(double2 (&r)[MS_N], const double *qp) {
   for (int j = 0; j < MS_N; ++j) {
     if ((j >> S) & 1) continue;
     if (C < MS_K && !((j >> C) & 1)) continue;
-    ms_pair<KIND>(r[j], r[j | (1 << S)], q);
+    spec_pair<KIND>(r[j], r[j | (1 << S)], q);
   }
 }
 
@@ -839,7 +847,7 @@ __device__ __forceinline__ void ms_dispatch(int code, double2 (&r)[MS_N], uint32
     break;
 #define MS_CASES_S(K_, S_) MS_CASE(K_, S_, 0) MS_CASE(K_, S_, 1) MS_CASE(K_, S_, 2) MS_CASE(K_, S_, 3)
 #define MS_CASES(K_) MS_CASES_S(K_, 0) MS_CASES_S(K_, 1) MS_CASES_S(K_, 2)
-    MS_CASES(MK_GENERAL) MS_CASES(MK_DIAG) MS_CASES(MK_PHASE) MS_CASES(MK_REAL) MS_CASES(MK_HSHARE)
+    MS_CASES(KIND_GENERAL) MS_CASES(KIND_DIAG) MS_CASES(KIND_PHASE) MS_CASES(KIND_REAL) MS_CASES(KIND_HSHARE)
 #undef MS_CASES
 #undef MS_CASES_S
 #undef MS_CASE
@@ -920,9 +928,15 @@ __device__ __noinline__ void ms_replay(double2 *__restrict__ a, uint64_t base, c
   for (int j = 0; j < MS_N; ++j) a[base | ms_off(j, b0, b1, b2)] = r[j];
 }
 
-__global__ void __launch_bounds__(BLK, SV_MS_MINB) k_mstage(double2 *__restrict__ a, uint64_t ngroups,
-                                                const __grid_constant__ MsParams P) {
-  const uint64_t p = (uint64_t)blockIdx.x * BLK + threadIdx.x;
+#ifndef SV_MS_BLK
+#define SV_MS_BLK 128  // measured 64/128/256/512: QFT(30) 87.9/86.1/87.0/90.1 ms
+#endif
+constexpr int MS_BLK = SV_MS_BLK;
+
+__global__ void __launch_bounds__(MS_BLK, SV_MS_MINB * 256 / MS_BLK) k_mstage(double2 *__restrict__ a,
+                                                                          uint64_t ngroups,
+                                                                          const __grid_constant__ MsParams P) {
+  const uint64_t p = (uint64_t)blockIdx.x * MS_BLK + threadIdx.x;
   const uint64_t b0 = 1ull << P.bits[0], b1 = 1ull << P.bits[1], b2 = 1ull << P.bits[2];
   const uint64_t base = insert_zero(insert_zero(insert_zero(p, P.bits[0]), P.bits[1]), P.bits[2]);
   const bool live = p < ngroups;
@@ -1175,6 +1189,14 @@ int launch_fused(double2 *a, int m, int T, const FusedParams &P, cudaStream_t st
   }
 }
 
+// Kind for the speculative fused kernels (tile, stage): KIND_* above.
+int gate_kind(const double *q) {
+  const bool z12 = q[2] == 0.0 && q[3] == 0.0, z21 = q[4] == 0.0 && q[5] == 0.0;
+  if (z12 && z21) return (q[0] == 1.0 && q[1] == 0.0) ? KIND_PHASE : KIND_DIAG;
+  if (!(q[1] == 0.0 && q[3] == 0.0 && q[5] == 0.0 && q[7] == 0.0)) return KIND_GENERAL;
+  return (q[0] == q[2] && q[0] == q[4] && q[0] == -q[6]) ? KIND_HSHARE : KIND_REAL;
+}
+
 int classify_kind(const double *q) {
   const bool z12 = q[2] == 0.0 && q[3] == 0.0, z21 = q[4] == 0.0 && q[5] == 0.0;
   if (!(z12 && z21)) return KIND_GENERAL;
@@ -1251,7 +1273,7 @@ int plan_tile(const sv_gate *gates, int n, int T, const int (&hb)[TR], TileParam
         G.cmode = 3;
         G.cabove = c;
       }
-      G.kind = (int8_t)classify_kind(src.q);
+      G.kind = (int8_t)gate_kind(src.q);
       memcpy(G.q, src.q, sizeof(G.q));
       ++gi;
     }
@@ -1322,13 +1344,6 @@ int stage_sig(const StageParams &P) {
   return 1;
 }
 
-int ms_kind(const double *q) {
-  const bool z12 = q[2] == 0.0 && q[3] == 0.0, z21 = q[4] == 0.0 && q[5] == 0.0;
-  if (z12 && z21) return (q[0] == 1.0 && q[1] == 0.0) ? MK_PHASE : MK_DIAG;
-  if (!(q[1] == 0.0 && q[3] == 0.0 && q[5] == 0.0 && q[7] == 0.0)) return MK_GENERAL;
-  return (q[0] == q[2] && q[0] == q[4] && q[0] == -q[6]) ? MK_HSHARE : MK_REAL;
-}
-
 // One multi-target stage launch: gates[0..n) with targets in <= MS_K bits.
 int run_mstage(double2 *a, int m, const sv_gate *gates, int n, cudaStream_t st) {
   static thread_local MsParams P;
@@ -1368,7 +1383,7 @@ int run_mstage(double2 *a, int m, const sv_gate *gates, int n, cudaStream_t st) 
   for (int k = 0; k < n; ++k) {
     const int c = gates[k].control, cs = c >= 0 ? slot(c) : MS_K;
     if (c >= 0 && cs == MS_K) P.cbit[k] = (uint8_t)c;
-    P.g[k].code = (ms_kind(gates[k].q) * MS_K + slot(gates[k].target)) * (MS_K + 1) + cs;
+    P.g[k].code = (gate_kind(gates[k].q) * MS_K + slot(gates[k].target)) * (MS_K + 1) + cs;
     P.g[k].pad = 0;
     memcpy(P.g[k].q, gates[k].q, sizeof(P.g[k].q));
   }
@@ -1386,7 +1401,7 @@ int run_mstage(double2 *a, int m, const sv_gate *gates, int n, cudaStream_t st) 
   }
   ++P.nruns;
   const uint64_t ng = 1ull << (m - MS_K);
-  k_mstage<<<grid_for(ng, BLK), BLK, 0, st>>>(a, ng, P);
+  k_mstage<<<grid_for(ng, MS_BLK), MS_BLK, 0, st>>>(a, ng, P);
   return after_launch("k_mstage");
 }
 
@@ -1396,18 +1411,22 @@ int run_mstage(double2 *a, int m, const sv_gate *gates, int n, cudaStream_t st) 
 // bits).  Candidate 2, a stage: the run whose targets stay within MS_K = 3
 // distinct bits.  Cost model (B200, ms at 2^30 amplitudes, compute overlapping
 // HBM): a pass costs max(5, sum of per-gate costs); per gate, tile 1.15
-// general / 0.45 diagonal, stage by structure (general 0.9, real 0.55,
-// Hadamard-like 0.35, diagonal 0.35, phase 0.18; half that when controlled).
+// general / 0.45 diagonal (real 0.75, Hadamard-like 0.55), stage by structure (general 0.9, real 0.55,
+// Hadamard-like 0.35, diagonal 0.35, phase 0.18; half that when controlled;
+// a stage with a target below bit 3 pays 1.7x for its strided loads).
 // The candidate with the lower cost per gate wins (ties: the stage).  A lone
 // gate is a single-gate launch.  Pure host code (sv_plan_gates exposes it).
 double stage_cost(const sv_gate &g) {
-  static const double c[MK_KINDS] = {0.9, 0.35, 0.18, 0.55, 0.35};
-  return c[ms_kind(g.q)] * (g.control >= 0 ? 0.5 : 1.0);
+  static const double c[KIND_COUNT] = {0.9, 0.35, 0.18, 0.55, 0.35};
+  return c[gate_kind(g.q)] * (g.control >= 0 ? 0.5 : 1.0);
 }
 
 int next_group(int m, const sv_gate *gates, int n, int i, int T, int *kind) {
   const int L = T - TR;
-  auto tile_cost = [&](int k) { return classify_kind(gates[k].q) == KIND_GENERAL ? 1.15 : 0.45; };
+  auto tile_cost = [&](int k) {
+    static const double c[KIND_COUNT] = {1.15, 0.45, 0.45, 0.75, 0.55};
+    return c[gate_kind(gates[k].q)];
+  };
   auto pass = [](double c) { return c > 5.0 ? c : 5.0; };
   int H[TR], nh = 0, ja = i;
   double ct = 0.0;
@@ -1438,6 +1457,9 @@ int next_group(int m, const sv_gate *gates, int n, int i, int T, int *kind) {
     }
   }
   const int A = ja - i, B = jb - i;
+  int lowest = 64;
+  for (int k = 0; k < ns; ++k) lowest = S[k] < lowest ? S[k] : lowest;
+  if (lowest < 3) cs = 1.7 * pass(cs);  // slot bits 0..2: 16-B pieces at 128-B strides per load (measured)
   if (A <= 1 && B <= 1) {
     *kind = SV_GROUP_GATES;
     return i + 1;

@@ -12,8 +12,9 @@ def test_qft_plan_is_one_pass_per_three_stages():
     n, m = 30, 30
     circ = sv.build_qft(n)
     plan = sv.plan_passes(circ.gates, m, 12)
-    # three consecutive transform stages H(k), R(k, c) for all c < k share one stage pass
-    assert [p.kind for p in plan] == ["local_stage"] * 10
+    # three consecutive transform stages H(k), R(k, c) for all c < k share one stage pass; the
+    # last three (targets 0..2, strided for a stage) go through the register tile
+    assert [p.kind for p in plan] == ["local_stage"] * 9 + ["local_tile"]
     assert [sorted({op.target for op in p.gates}) for p in plan] == [[k - 2, k - 1, k] for k in range(29, 0, -3)]
     assert [op for p in plan for op in p.gates] == list(circ.gates)
     assert max(len(p.gates) for p in plan) <= sv._lib.SV_MSTAGE_MAX_GATES
