@@ -232,6 +232,30 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+# FP64 pipe ops per pair of the cheapest exact update each gate shape admits (svb200.cu spec_pair):
+# general mix() 20, real 12, Hadamard-like 8, diagonal 8, phase 4 (one cmul on the |1> side).
+FP64_OPS = {"general": 20, "real": 12, "hshare": 8, "diag": 8, "phase": 4}
+FP64_PEAK_OPS = 17.0e12  # measured DFMA/DMUL issue rate, tools/micro/fp64_probe.cu
+
+
+def gate_shape(q) -> str:
+    q = np.asarray(q, dtype=np.complex128).reshape(2, 2)
+    if q[0, 1] == 0 and q[1, 0] == 0:
+        return "phase" if q[0, 0] == 1 else "diag"
+    if np.all(q.imag == 0):
+        return "hshare" if q[0, 0] == q[0, 1] == q[1, 0] == -q[1, 1] else "real"
+    return "general"
+
+
+def fp64_ops(gates, m) -> int:
+    """Algorithmic FP64 ops of a gate list on a 2^m slice (local gates; controls halve the pairs)."""
+    tot = 0
+    for op in gates:
+        pairs = 1 << (m - 1 - (op.control is not None))
+        tot += FP64_OPS[gate_shape(op.gate.mat if hasattr(op.gate, "mat") else op.gate)] * pairs
+    return tot
+
+
 def make_units(sv, circ, m, fusion, l_c, state, fabric):
     """The launch groups of one step: (kind, algorithmic HBM bytes, gate count, callable).
 
@@ -242,7 +266,7 @@ def make_units(sv, circ, m, fusion, l_c, state, fabric):
 
         tile = tile_for(l_c, m)
         return [("pass-" + p.kind, 32 << m, len(p.gates),
-                 (lambda p=p: sv.execute_pass(state, p, fabric, tile=tile)))
+                 (lambda p=p: sv.execute_pass(state, p, fabric, tile=tile)), p.gates)
                 for p in sv.plan_passes(circ.gates, m, tile)]
     units = []
     for op in circ:
@@ -253,14 +277,14 @@ def make_units(sv, circ, m, fusion, l_c, state, fabric):
             kind, nbytes = "controlled", 16 << m
         else:
             kind, nbytes = "exchange", sv.link_bytes_per_direction(case, m)
-        units.append((kind, nbytes, 1, (lambda op=op: sv.apply_op(state, op, fabric))))
+        units.append((kind, nbytes, 1, (lambda op=op: sv.apply_op(state, op, fabric)), (op,)))
     return units
 
 
 KERNELS = {
     "single": ("sv_apply_single", "k_pairs/k_shfl<MODE_SINGLE> (sv_apply_single)"),
     "controlled": ("sv_apply_controlled", "k_pairs/k_shfl<MODE_CTL|MODE_PRED> (sv_apply_controlled)"),
-    "pass-local_stage": ("sv_apply_gates:stage", "k_stage_pairs (sv_apply_gates, same-target stage pass)"),
+    "pass-local_stage": ("sv_apply_gates:stage", "k_mstage (sv_apply_gates, multi-target stage pass)"),
     "pass-local_tile": ("sv_apply_gates:tile", "k_tile (sv_apply_gates, register-tiled run)"),
     "pass-local_gate": ("sv_apply_single", "k_pairs/k_shfl (single gate of a pass plan)"),
 }
@@ -318,7 +342,7 @@ def main():
 
     # ---------------------------------------------------------- warm-up
     for c in circs[: args.warmup]:
-        for _, _, _, fn in make_units(sv, c, m, fusion, args.l_c, state, fabric):
+        for _, _, _, fn, _ in make_units(sv, c, m, fusion, args.l_c, state, fabric):
             fn()
     barrier()
 
@@ -335,7 +359,7 @@ def main():
         for us in units:
             row = [torch.cuda.Event(enable_timing=True)]
             row[0].record(stream)
-            for _, _, _, fn in us:
+            for _, _, _, fn, _ in us:
                 fn()
                 e = torch.cuda.Event(enable_timing=True)
                 e.record(stream)
@@ -357,25 +381,30 @@ def main():
     peaks, peak_kind = load_peaks()
     by_kind: dict = {}
     for us, ms in zip(units, unit_ms):
-        for (kind, nbytes, cnt, _), t_ms in zip(us, ms):
-            by_kind.setdefault(kind, []).append((nbytes, t_ms, cnt))
+        for (kind, nbytes, cnt, _, gates), t_ms in zip(us, ms):
+            by_kind.setdefault(kind, []).append((nbytes, t_ms, cnt, gates))
     local_kinds = [k for k in by_kind if k in KERNELS]
     roof = None
     if local_kinds:
-        top = max(local_kinds, key=lambda k: sum(t for _, t, _ in by_kind[k]))
+        top = max(local_kinds, key=lambda k: sum(r[1] for r in by_kind[k]))
         rows = by_kind[top]
-        avg_ms = float(np.mean([t for _, t, _ in rows]))
-        alg = int(np.mean([b for b, _, _ in rows]))
+        avg_ms = float(np.mean([r[1] for r in rows]))
+        alg = int(np.mean([r[0] for r in rows]))
         achieved = alg / (avg_ms * 1e-3) / 1e9
         key, kname = KERNELS[top]
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": ncu_traffic(key, alg),
                 "kernel": kname, "peak_kind": peak_kind, "algorithmic_bytes_per_launch": alg,
                 "avg_launch_ms": round(avg_ms, 4), "launches": len(rows),
-                "share_of_step": round(sum(t for _, t, _ in rows) / elapsed_ms, 4),
+                "share_of_step": round(sum(r[1] for r in rows) / elapsed_ms, 4),
                 "frac_of_8TBs": round(achieved / 8000.0, 4)}
         if top.startswith("pass-"):
-            roof["gates_per_launch"] = round(float(np.mean([c for _, _, c in rows])), 2)
+            roof["gates_per_launch"] = round(float(np.mean([r[2] for r in rows])), 2)
+            # fused passes are FP64-pipe bound once a pass carries enough gates: report that roofline too
+            ops = float(np.mean([fp64_ops(r[3], m) for r in rows]))
+            roof["fp64"] = {"achieved_tops": round(ops / (avg_ms * 1e-3) / 1e12, 3),
+                            "peak_tops": FP64_PEAK_OPS / 1e12, "frac": round(ops / (avg_ms * 1e-3) / FP64_PEAK_OPS, 4),
+                            "ops_per_launch": int(ops), "peak_kind": "measured (tools/micro/fp64_probe.cu)"}
     per_target = {}
     if args.workload == "sweep" and fusion == "none":
         for k in range(m):

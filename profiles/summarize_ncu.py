@@ -25,6 +25,8 @@ METRICS = [
     "launch__registers_per_thread", "launch__grid_size", "launch__block_size", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
     "lts__t_sectors_srcunit_tex_op_read.sum", "lts__t_sectors_srcunit_tex_op_write.sum",
     "launch__occupancy_limit_registers", "smsp__inst_executed.sum", "lts__t_sector_hit_rate.pct",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
 ]
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
          "ns": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3, "s": 1, "second": 1}
@@ -71,6 +73,8 @@ def main():
     ap.add_argument("--launches")
     ap.add_argument("--rep", action="append", default=[])
     ap.add_argument("--note", default="")
+    ap.add_argument("--out", default=None, help="markdown name (default <round>_ncu.md)")
+    ap.add_argument("--alg-bytes", type=float, default=None, help="algorithmic bytes per launch of the captures")
     a = ap.parse_args()
     md = [f"# ncu summary {a.round}", "", a.note, ""]
     if a.launches:
@@ -95,7 +99,9 @@ def main():
                                         "registers": d.get("launch__registers_per_thread"),
                                         "dram_pct_peak": d.get(
                                             "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed")}
-    (HERE / f"{a.round}_ncu.md").write_text("\n".join(md) + "\n")
+                if a.alg_bytes:
+                    summ["kernels"][key]["algorithmic_bytes"] = int(a.alg_bytes)
+    (HERE / (a.out or f"{a.round}_ncu.md")).write_text("\n".join(md) + "\n")
     summ_path.write_text(json.dumps(summ, indent=1) + "\n")
     print("\n".join(md))
 
