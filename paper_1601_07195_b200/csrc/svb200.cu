@@ -1387,10 +1387,15 @@ int run_mstage(double2 *a, int m, const sv_gate *gates, int n, cudaStream_t st) 
     P.g[k].pad = 0;
     memcpy(P.g[k].q, gates[k].q, sizeof(P.g[k].q));
   }
+  // Runs split where the control moves between lane bits (per-lane test) and the rest, so the
+  // kernel runs the test-free loop for every run without lane-bit controls.
+  uint64_t lanes = 0x1F;  // slice bits that differ across the 32 lanes of a warp
+  for (int s = 0; s < MS_K; ++s) lanes = ((lanes >> bits[s]) << (bits[s] + 1)) | (lanes & ((1ull << bits[s]) - 1));
+  auto lane_dep = [&](int k) { return P.cbit[k] != 0xFF && ((lanes >> P.cbit[k]) & 1ull); };
   P.nruns = 0;
   for (int k = 0; k < n; ++k) {
     MsRun &R = P.run[P.nruns];
-    const bool extend = k > 0 && R.code == P.g[k].code && R.h == k / 32;
+    const bool extend = k > 0 && R.code == P.g[k].code && R.h == k / 32 && lane_dep(k) == lane_dep(k - 1);
     if (!extend) {
       MsRun &N = P.run[k > 0 ? ++P.nruns : P.nruns];
       N.code = (uint8_t)P.g[k].code;
