@@ -230,6 +230,8 @@ def run_reference(args):
         "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+    if args.out:
+        Path(args.out).write_text(json.dumps(line) + "\n")
 
 
 # FP64 pipe ops per pair of the cheapest exact update each gate shape admits (svb200.cu spec_pair):

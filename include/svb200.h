@@ -82,8 +82,9 @@ int sv_apply_fused(void *amps, int m, int l, const sv_gate *gates, int ngates, v
  * controls < m) in order, grouping it into as few HBM passes as the kernels
  * allow -- maximal runs of gates with target < tile (controls anywhere: above
  * the tile they are per-CTA predicates) go through the register-tiled kernel;
- * maximal runs sharing one higher target go through one same-target stage
- * pass; anything else is a single-gate launch.  Bit-identical to applying the
+ * runs whose targets lie in at most SV_MSTAGE_MAX_TARGETS qubits go through one
+ * multi-target stage pass (whichever covers a run more cheaply, by a B200 cost
+ * model); anything else is a single-gate launch.  Bit-identical to applying the
  * gates one by one with sv_apply_single / sv_apply_controlled (the reference's
  * engine.py:88-95 loop).  tile = 0 picks min(m, SV_FUSED_MAX_TILE); otherwise
  * 9 <= tile <= min(m, SV_FUSED_MAX_TILE). */
