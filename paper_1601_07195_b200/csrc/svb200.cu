@@ -260,8 +260,18 @@ template <int KIND>
 __device__ __forceinline__ void pair_update(double2 &a0, double2 &a1, const double *q) {
   double2 n0, n1;
   if (KIND == KIND_GENERAL) {
-    n0 = mix(a0, a1, q[0], q[1], q[2], q[3]);
-    n1 = mix(a0, a1, q[4], q[5], q[6], q[7]);
+    // mix() for both outputs, every product formed first, then the fmas, then the adds (the
+    // same rounding sequence; the order only helps ptxas keep a0/a1 in their registers)
+    const double t0 = __dmul_rn(a0.y, q[1]), t1 = __dmul_rn(a0.x, q[1]);
+    const double t2 = __dmul_rn(a1.y, q[3]), t3 = __dmul_rn(a1.x, q[3]);
+    const double t4 = __dmul_rn(a0.y, q[5]), t5 = __dmul_rn(a0.x, q[5]);
+    const double t6 = __dmul_rn(a1.y, q[7]), t7 = __dmul_rn(a1.x, q[7]);
+    const double p0r = __fma_rn(q[0], a0.x, -t0), p0i = __fma_rn(q[0], a0.y, t1);
+    const double p1r = __fma_rn(q[2], a1.x, -t2), p1i = __fma_rn(q[2], a1.y, t3);
+    const double p2r = __fma_rn(q[4], a0.x, -t4), p2i = __fma_rn(q[4], a0.y, t5);
+    const double p3r = __fma_rn(q[6], a1.x, -t6), p3i = __fma_rn(q[6], a1.y, t7);
+    n0 = make_double2(__dadd_rn(p0r, p1r), __dadd_rn(p0i, p1i));
+    n1 = make_double2(__dadd_rn(p2r, p3r), __dadd_rn(p2i, p3i));
   } else {
     if (KIND == KIND_PHASE && nonzero2(a0))
       n0 = a0;
@@ -384,25 +394,12 @@ __device__ __forceinline__ int reg_off(int j, const int m0, const int m1, const 
 // branch (see stage_gate).  FULL: every pair active (pm == 0xFFFF).
 constexpr int TG = 2;
 
-// spec (speculative pass, warp-uniform): diagonal/phase gates update in place
-// with their products only; k_tile tests the final tile once and replays it
-// from global memory with spec = false if any component is zero (see
-// stage_gate_fast for why that one test is enough).
-template <int TB, int KIND, bool FULL, bool SPEC>
-__device__ __forceinline__ void tile_gate_k(double2 (&r)[TRN], uint32_t pm, const double *qp) {
-  double q[8];  // once per gate in registers, not one constant-bank load per pair
-#pragma unroll
-  for (int i = 0; i < 8; ++i) q[i] = qp[i];
 #define PAIRS(k) ((((k) >> TB) << (TB + 1)) | ((k) & ((1 << TB) - 1)))  // k-th j with bit TB clear
-  if (KIND != KIND_GENERAL && SPEC) {
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int j = PAIRS(k);
-      if (!(FULL || ((pm >> j) & 1u))) continue;
-      spec_pair<KIND>(r[j], r[j | (1 << TB)], q);
-    }
-    return;
-  }
+
+// The exact update of one register bit's 8 pairs (mix() for general and real kinds; diagonal
+// and phase kinds with per-group zero tests).
+template <int TB, int KIND, bool FULL>
+__device__ __forceinline__ void tile_gate_exact(double2 (&r)[TRN], uint32_t pm, const double *q) {
 #pragma unroll
   for (int grp = 0; grp < 8 / TG; ++grp) {
     if (KIND == KIND_GENERAL || KIND >= KIND_REAL) {  // exact pass: real kinds run mix()
@@ -439,6 +436,27 @@ __device__ __forceinline__ void tile_gate_k(double2 (&r)[TRN], uint32_t pm, cons
         }
       }
     }
+  }
+}
+
+// spec (speculative pass, warp-uniform): diagonal/phase gates update in place
+// with their products only; k_tile tests the final tile once and replays it
+// from global memory with spec = false if any component is zero (see
+// stage_gate_fast for why that one test is enough).
+template <int TB, int KIND, bool FULL, bool SPEC>
+__device__ __forceinline__ void tile_gate_k(double2 (&r)[TRN], uint32_t pm, const double *qp) {
+  double q[8];  // once per gate in registers, not one constant-bank load per pair
+#pragma unroll
+  for (int i = 0; i < 8; ++i) q[i] = qp[i];
+  if (KIND != KIND_GENERAL && SPEC) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int j = PAIRS(k);
+      if (!(FULL || ((pm >> j) & 1u))) continue;
+      spec_pair<KIND>(r[j], r[j | (1 << TB)], q);
+    }
+  } else {
+    tile_gate_exact<TB, KIND, FULL>(r, pm, q);
   }
 }
 
