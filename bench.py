@@ -429,7 +429,7 @@ def main():
     glob = [r for k, rs in by_kind.items() if k in ("exchange", "pass-global_stage", "pass-global_gate") for r in rs]
     if world > 1 and glob:
         per_dir = 1 << (m + 4)
-        d = float(np.mean([t for _, t, _ in glob]))
+        d = float(np.mean([r[1] for r in glob]))
         nvlink = {"achieved_gbs_per_direction": round(per_dir / (d * 1e-3) / 1e9, 1),
                   "peak_nominal": 900.0, "peak_measured_ref": 770.0,
                   "frac_nominal": round(per_dir / (d * 1e-3) / 1e9 / 900.0, 4),
