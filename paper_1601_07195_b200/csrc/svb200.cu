@@ -581,11 +581,13 @@ __global__ void __launch_bounds__(1 << (T - TR), (T <= 12) ? 2 : 1)
   for (int j = 0; j < TRN; ++j) a[tile0 + tile_off<T>(tid, j, hb)] = r[j];
 }
 
-// ------------------------------------------------------------ same-target stages
+// ------------------------------------------------- same-target stages (exchange)
 //
-// A run of gates sharing one target k (any controls, any structure) in one HBM
-// pass: each thread keeps its pairs (i, i + 2^k) in registers and applies the
-// whole list in order -- e.g. a transform stage H(k), R(k, c) for every c < k.
+// A run of gates sharing one target (any controls, any structure) applied to
+// pairs held in registers, in order -- e.g. a transform stage H(k), R(k, c) for
+// every c < k.  Used by k_exchange_stage, where the target is a global qubit
+// and the pair is (own element, partner element over NVLink); local stages go
+// through k_mstage.  SUNROLL pairs per thread.
 
 constexpr int STAGE_MAX_GATES = 64;
 
@@ -603,7 +605,7 @@ struct StageParams {
 };
 
 #ifndef SV_SUNROLL
-#define SV_SUNROLL 2  // measured best of 1/2/4/8 on B200 (more resident warps hide the per-gate chains)
+#define SV_SUNROLL 2  // measured best of 1/2/4/8 for the former local stage kernel (resident warps hide the per-gate chains)
 #endif
 constexpr int SUNROLL = SV_SUNROLL;
 
