@@ -330,6 +330,9 @@ __device__ __forceinline__ void spec_pair(double2 &a0, double2 &a1, const double
 // one stores straight to global when it ends in that layout.
 
 constexpr int TR = 4;
+#ifndef SV_TILE_MINB
+#define SV_TILE_MINB 2  // CTAs per SM for T <= 12 tiles (measured: 1 CTA with 255 registers is 1.6x slower)
+#endif
 constexpr int TRN = 1 << TR;
 constexpr int TILE_MAX_GATES = 256;
 constexpr int TILE_MAX_SEGS = 64;
@@ -558,7 +561,7 @@ __device__ __noinline__ void tile_replay(double2 *__restrict__ a, uint64_t tile0
 // zero component the whole tile is replayed exactly from global memory
 // (nothing has been stored yet).  SPEC = false: the exact path.
 template <int T, bool SPEC>
-__global__ void __launch_bounds__(1 << (T - TR), (T <= 12) ? 2 : 1)
+__global__ void __launch_bounds__(1 << (T - TR), (T <= 12) ? SV_TILE_MINB : 1)
     k_tile(double2 *__restrict__ a, const __grid_constant__ TileParams P) {
   extern __shared__ double2 s[];
   int hb[TR];
