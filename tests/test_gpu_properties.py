@@ -107,3 +107,36 @@ def test_long_circuit_norm_n20():
         s = sv.init_basis_state(sv.Layout(20), device=DEV)
         sv.run_circuit(s, circ, fusion=sv.FusionConfig(l_c=13, passes=True))
         assert abs(1.0 - sv.global_norm_sq(s)) <= 1e-10
+
+
+@given(st.integers(9, 16), st.integers(0, 2**31 - 1), st.sampled_from([0, 9, 10, 12]),
+       st.floats(0.0, 0.6), st.booleans())
+@settings(max_examples=40, deadline=None)
+def test_native_planner_bitwise_fuzz(n, seed, tile, zero_frac, structured):
+    """sv_apply_gates on random gate lists (every update shape, controls anywhere, runs that
+    favour stages or tiles, states salted with +-0) equals the oracle's unfused, unspecialised
+    evaluation bit for bit -- tiles, multi-target stages, speculation and replays included."""
+    from oracle import oracle
+
+    rng = np.random.default_rng(seed)
+    v = random_state(rng, n)
+    if zero_frac:
+        f = v.view(np.float64)
+        hit = rng.random(f.shape) < zero_frac
+        f[hit] = np.where(rng.random(hit.sum()) < 0.5, 0.0, -0.0)
+    th = float(rng.uniform(0, 2 * np.pi))
+    zoo = [sv.random_unitary(rng), sv.hadamard(), sv.phase_r(int(rng.integers(1, 9))), sv.pauli_z(),
+           sv.pauli_x(), sv.rotation_y(th), sv.rotation_z(th), sv.GateMatrix.unchecked([[1, 0], [0, 0.5 + 0.5j]]),
+           sv.GateMatrix.unchecked([[0.5, 0.5], [0.5, -0.5]])]
+    hot = [int(x) for x in rng.choice(n, 3, replace=False)]
+    ops = []
+    for _ in range(int(rng.integers(1, 160))):
+        t = hot[int(rng.integers(3))] if structured and rng.random() < 0.8 else int(rng.integers(n))
+        c = None if rng.random() < 0.4 else int((t + 1 + rng.integers(n - 1)) % n)
+        ops.append(sv.GateOp(zoo[int(rng.integers(len(zoo)))], t, c))
+    T = tile if tile and tile <= min(n, 13) else 0
+    a = dev(v)
+    sv.kernels.apply_gates(a, ops, tile=T)
+    w = v.copy()
+    oracle.run_circuit(w, ops, threads=4)
+    assert np.array_equal(host(a).view(np.uint64), w.view(np.uint64))
