@@ -329,11 +329,25 @@ __device__ __forceinline__ void spec_pair(double2 &a0, double2 &a1, const double
 // global load when its register set is the top four tile bits, and the last
 // one stores straight to global when it ends in that layout.
 
-constexpr int TR = 4;
+#ifndef SV_TILE_TR
+#define SV_TILE_TR 4  // register qubits per thread; TR = 3 measured slower (random 64-gate run 81 vs 66 ms)
+#endif
+constexpr int TR = SV_TILE_TR;
+static_assert(TR == 3 || TR == 4, "tile register bits");
 #ifndef SV_TILE_MINB
 #define SV_TILE_MINB 2  // CTAs per SM for T <= 12 tiles (measured: 1 CTA with 255 registers is 1.6x slower)
 #endif
 constexpr int TRN = 1 << TR;
+constexpr uint32_t TFULL = (1u << TRN) - 1u;  // every register pair of a gate active
+
+// registers j whose register bit b is set (a control on register bit b)
+__host__ __device__ constexpr uint32_t reg_mask(int b) {
+  return TFULL & (b == 0 ? 0xAAAAu : b == 1 ? 0xCCCCu : b == 2 ? 0xF0F0u : 0xFF00u);
+}
+
+struct TileHB {
+  int v[TR];
+};
 constexpr int TILE_MAX_GATES = 256;
 constexpr int TILE_MAX_SEGS = 64;
 
@@ -347,7 +361,7 @@ struct TileGate {
 };
 
 struct TileSeg {
-  uint8_t S[TR];      // tile bits held in register bits 0..3 (ascending)
+  uint8_t S[4];       // tile bits held in register bits 0..TR-1 (ascending)
   uint8_t tbits[12];  // tile bit of thread-index bit b
   int16_t first, count;
   int8_t natural, pad[3];
@@ -377,8 +391,10 @@ __device__ __forceinline__ uint64_t tile_base(uint64_t b, const int (&hb)[TR]) {
 // slice offset (relative to the tile base) of natural-layout register j of thread tid
 template <int T>
 __device__ __forceinline__ uint64_t tile_off(int tid, int j, const int (&hb)[TR]) {
-  return (uint64_t)tid | ((uint64_t)(j & 1) << hb[0]) | ((uint64_t)((j >> 1) & 1) << hb[1]) |
-         ((uint64_t)((j >> 2) & 1) << hb[2]) | ((uint64_t)((j >> 3) & 1) << hb[3]);
+  uint64_t o = (uint64_t)tid;
+#pragma unroll
+  for (int k = 0; k < TR; ++k) o |= (uint64_t)((j >> k) & 1) << hb[k];
+  return o;
 }
 
 __device__ __forceinline__ int swz(int i) {
@@ -388,13 +404,16 @@ __device__ __forceinline__ int swz(int i) {
   return i ^ (h & 7);
 }
 
-__device__ __forceinline__ int reg_off(int j, const int m0, const int m1, const int m2, const int m3) {
-  return ((j & 1) ? m0 : 0) | ((j & 2) ? m1 : 0) | ((j & 4) ? m2 : 0) | ((j & 8) ? m3 : 0);
+__device__ __forceinline__ int reg_off(int j, const int (&m)[TR]) {
+  int o = 0;
+#pragma unroll
+  for (int k = 0; k < TR; ++k) o |= ((j >> k) & 1) ? m[k] : 0;
+  return o;
 }
 
-// The 8 register pairs of a gate on register bit TB, processed in groups of
-// TG; for diagonal/phase gates the zero tests of a group are merged into one
-// branch (see stage_gate).  FULL: every pair active (pm == 0xFFFF).
+// The TRN/2 register pairs of a gate on register bit TB, processed in groups
+// of TG; for diagonal/phase gates the zero tests of a group are merged into
+// one branch (see stage_gate).  FULL: every pair active (pm == TFULL).
 constexpr int TG = 2;
 
 #define PAIRS(k) ((((k) >> TB) << (TB + 1)) | ((k) & ((1 << TB) - 1)))  // k-th j with bit TB clear
@@ -404,7 +423,7 @@ constexpr int TG = 2;
 template <int TB, int KIND, bool FULL>
 __device__ __forceinline__ void tile_gate_exact(double2 (&r)[TRN], uint32_t pm, const double *q) {
 #pragma unroll
-  for (int grp = 0; grp < 8 / TG; ++grp) {
+  for (int grp = 0; grp < TRN / 2 / TG; ++grp) {
     if (KIND == KIND_GENERAL || KIND >= KIND_REAL) {  // exact pass: real kinds run mix()
 #pragma unroll
       for (int k = 0; k < TG; ++k) {
@@ -453,7 +472,7 @@ __device__ __forceinline__ void tile_gate_k(double2 (&r)[TRN], uint32_t pm, cons
   for (int i = 0; i < 8; ++i) q[i] = qp[i];
   if (KIND != KIND_GENERAL && SPEC) {
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
+    for (int k = 0; k < TRN / 2; ++k) {
       const int j = PAIRS(k);
       if (!(FULL || ((pm >> j) & 1u))) continue;
       spec_pair<KIND>(r[j], r[j | (1 << TB)], q);
@@ -467,7 +486,7 @@ template <int TB, bool SPEC>
 __device__ __forceinline__ void tile_gate(double2 (&r)[TRN], uint32_t pm, int kind, const double *q) {
   if (pm == 0u) return;
   if (!SPEC && kind >= KIND_REAL) kind = KIND_GENERAL;  // the exact pass runs mix() for them
-  if (pm == 0xFFFFu) {  // uncontrolled, or control decided per thread/CTA: straight-line code
+  if (pm == TFULL) {  // uncontrolled, or control decided per thread/CTA: straight-line code
     switch (kind) {
       case KIND_GENERAL: tile_gate_k<TB, KIND_GENERAL, true, SPEC>(r, pm, q); break;
       case KIND_PHASE: tile_gate_k<TB, KIND_PHASE, true, SPEC>(r, pm, q); break;
@@ -494,47 +513,52 @@ __device__ __forceinline__ void tile_body(const double2 *__restrict__ a, uint64_
   constexpr int NT = 1 << (T - TR);
 #pragma unroll
   for (int j = 0; j < TRN; ++j) r[j] = a[tile0 + tile_off<T>(tid, j, hb)];
-  // current layout: natural (register bits = top four tile bits, thread bits ascending)
-  int cbase = tid, c0 = NT, c1 = NT << 1, c2 = NT << 2, c3 = NT << 3;
+  // current layout: natural (register bits = top TR tile bits, thread bits ascending)
+  int cbase = tid, c[TR];
+#pragma unroll
+  for (int k = 0; k < TR; ++k) c[k] = NT << k;
   bool touched = false;
   for (int sg = 0; sg < P.nsegs; ++sg) {
     const TileSeg &S = P.seg[sg];
-    const int m0 = 1 << S.S[0], m1 = 1 << S.S[1], m2 = 1 << S.S[2], m3 = 1 << S.S[3];
+    int mm[TR];
+#pragma unroll
+    for (int k = 0; k < TR; ++k) mm[k] = 1 << S.S[k];
     int base = 0;
 #pragma unroll
     for (int b = 0; b < T - TR; ++b) base |= ((tid >> b) & 1) << S.tbits[b];
     if (!(sg == 0 && S.natural)) {
       if (touched) __syncthreads();
 #pragma unroll
-      for (int j = 0; j < TRN; ++j) s[swz(cbase | reg_off(j, c0, c1, c2, c3))] = r[j];
+      for (int j = 0; j < TRN; ++j) s[swz(cbase | reg_off(j, c))] = r[j];
       __syncthreads();
 #pragma unroll
-      for (int j = 0; j < TRN; ++j) r[j] = s[swz(base | reg_off(j, m0, m1, m2, m3))];
+      for (int j = 0; j < TRN; ++j) r[j] = s[swz(base | reg_off(j, mm))];
       touched = true;
     }
     cbase = base;
-    c0 = m0, c1 = m1, c2 = m2, c3 = m3;
+#pragma unroll
+    for (int k = 0; k < TR; ++k) c[k] = mm[k];
     for (int gi = S.first; gi < S.first + S.count; ++gi) {
       const TileGate &G = P.g[gi];
-      uint32_t pm = 0xFFFFu;
+      uint32_t pm = TFULL;
       if (G.cmode == 1)
-        pm = G.cbit == 0 ? 0xAAAAu : G.cbit == 1 ? 0xCCCCu : G.cbit == 2 ? 0xF0F0u : 0xFF00u;
+        pm = G.cbit == 0 ? reg_mask(0) : G.cbit == 1 ? reg_mask(1) : G.cbit == 2 ? reg_mask(2) : reg_mask(3);
       else if (G.cmode == 2)
-        pm = ((base >> G.cbit) & 1) ? 0xFFFFu : 0u;
+        pm = ((base >> G.cbit) & 1) ? TFULL : 0u;
       else if (G.cmode == 3)
-        pm = ((tile0 >> G.cabove) & 1ull) ? 0xFFFFu : 0u;
+        pm = ((tile0 >> G.cabove) & 1ull) ? TFULL : 0u;
       switch (G.tb) {
         case 0: tile_gate<0, SPEC>(r, pm, G.kind, G.q); break;
         case 1: tile_gate<1, SPEC>(r, pm, G.kind, G.q); break;
         case 2: tile_gate<2, SPEC>(r, pm, G.kind, G.q); break;
-        default: tile_gate<3, SPEC>(r, pm, G.kind, G.q); break;
+        default: tile_gate<TR - 1, SPEC>(r, pm, G.kind, G.q); break;
       }
     }
   }
   if (!P.last_natural) {
     if (touched) __syncthreads();
 #pragma unroll
-    for (int j = 0; j < TRN; ++j) s[swz(cbase | reg_off(j, c0, c1, c2, c3))] = r[j];
+    for (int j = 0; j < TRN; ++j) s[swz(cbase | reg_off(j, c))] = r[j];
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < TRN; ++j) r[j] = s[swz(tid + j * NT)];
@@ -546,9 +570,11 @@ __device__ __forceinline__ void tile_body(const double2 *__restrict__ a, uint64_
 // the body in its register allocation (inlined, the pair spilled ~3 KB per
 // thread at the 128-register cap); the call site keeps only a few scalars live.
 template <int T>
-__device__ __noinline__ void tile_replay(double2 *__restrict__ a, uint64_t tile0, int hb0, int hb1, int hb2,
-                                         int hb3, const TileParams *P, double2 *s) {
-  const int hb[TR] = {hb0, hb1, hb2, hb3};
+__device__ __noinline__ void tile_replay(double2 *__restrict__ a, uint64_t tile0, TileHB h, const TileParams *P,
+                                         double2 *s) {
+  int hb[TR];
+#pragma unroll
+  for (int k = 0; k < TR; ++k) hb[k] = h.v[k];
   const int tid = threadIdx.x;
   double2 r[TRN];
   tile_body<T, false>(a, tile0, hb, tid, *P, s, r);
@@ -576,7 +602,10 @@ __global__ void __launch_bounds__(1 << (T - TR), (T <= 12) ? SV_TILE_MINB : 1)
 #pragma unroll
     for (int j = 0; j < TRN; ++j) ok &= nonzero2(r[j]);
     if (__syncthreads_or(!ok)) {
-      tile_replay<T>(a, tile0, hb[0], hb[1], hb[2], hb[3], &P, s);
+      TileHB h;
+#pragma unroll
+      for (int k = 0; k < TR; ++k) h.v[k] = hb[k];
+      tile_replay<T>(a, tile0, h, &P, s);
       return;
     }
   }
@@ -1612,7 +1641,8 @@ int sv_apply_fused(void *amps, int m, int l, const sv_gate *gates, int ngates, v
   // SM overlap one tile's HBM traffic with the other's gates), never below l.
   const int T = l > 12 ? l : (m < 12 ? m : 12);
   if (T >= 9) {
-    const int hb[TR] = {T - 4, T - 3, T - 2, T - 1};  // contiguous 2^T blocks
+    int hb[TR];  // contiguous 2^T blocks
+    for (int k = 0; k < TR; ++k) hb[k] = T - TR + k;
     return run_tile((double2 *)amps, m, T, hb, gates, ngates, (cudaStream_t)stream);
   }
   static thread_local FusedParams P;  // 18 KB: keep it off the stack
