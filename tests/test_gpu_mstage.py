@@ -108,3 +108,17 @@ def test_stage_abi_guards():
     many = [sv.GateOp(sv.hadamard(), 1)] * (_lib.SV_MSTAGE_MAX_GATES + 1)
     assert L.sv_apply_group(ptr, m, _lib.SV_GROUP_STAGE, gate_array(many), len(many), 0,
                             stream_handle()) == _lib.SV_EINVAL
+
+
+@pytest.mark.parametrize("n", [3, 4, 5, 6, 7])
+def test_stage_tiny_slices_partial_warps(n):
+    """Slices with fewer than 32 groups (partial warps take part in the ballots with dummy rows)."""
+    rng = np.random.default_rng(600 + n)
+    for trial in range(4):
+        v = with_zeros(rng, n) if trial % 2 else random_state(rng, n)
+        targets = [int(t) for t in rng.choice(n, min(3, n), replace=False)]
+        ops = stage_ops(rng, n, targets, [5, 40, 77, 128][trial])
+        a = torch.from_numpy(v.copy()).to(DEV)
+        apply_stage(a, ops)
+        torch.cuda.synchronize()
+        assert bits_equal(a.cpu().numpy(), run_oracle(v, ops)), (n, trial)
