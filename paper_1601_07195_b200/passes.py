@@ -8,9 +8,11 @@ allow, without reordering any gate:
 * ``local`` pass -- a maximal run of gates with a local target (controls
   anywhere; a control in the rank bits turns into "uncontrolled" or "skip" on
   this rank).  Executed by ``sv_apply_gates``: register-tiled runs for
-  targets below the tile (2^13), one same-target stage pass for each run of
-  gates sharing a higher target (a transform stage H(k), R(k, c) for all c
-  is ONE pass), single-gate kernels otherwise.
+  targets below the tile (2^12) plus up to four gathered higher qubits,
+  multi-target stage passes for runs whose targets lie in at most three qubits
+  (three transform stages H(k), R(k, c) for all c are ONE pass), single-gate
+  kernels otherwise -- whichever covers the run more cheaply (svb200.cu
+  ``next_group``).
 * ``global_stage`` -- a run of gates sharing one global target: ONE fused
   NVLink exchange applies them all (``sv_exchange_stage``).
 * ``global_gate`` -- a lone global-target gate: the reference-equivalent
@@ -18,7 +20,9 @@ allow, without reordering any gate:
 
 Results are bit-identical to the reference's unfused execution: every pair
 sees the same updates in the same order, and the structure-specialised
-updates (diagonal / phase gates) are exact (svb200.cu "pair update").
+updates (diagonal / phase / real / Hadamard-like gates) are exact -- they
+differ from mix() only in zero signs, and any zero in a pass's final values
+sends that group through an exact replay (svb200.cu "speculative pair updates").
 """
 
 from __future__ import annotations
@@ -51,10 +55,9 @@ def plan_passes(gates, m: int, tile: int = 0) -> list[Pass]:
     """Cut a gate sequence into HBM passes -- a pure function of the gates, m and the tile,
     so every rank derives the same list (the collective fences line up).
 
-    Local targets: a maximal run of targets below the register tile is one
-    ``local_tile`` pass; a maximal run sharing one higher target is one
-    ``local_stage`` pass; a lone gate is a ``local_gate``.  Global targets: a
-    run sharing the target is one ``global_stage`` exchange.  This is the
+    Local targets: the native planner's groups (``sv_plan_gates``): a register-tiled
+    ``local_tile`` pass, a multi-target ``local_stage`` pass, or a lone ``local_gate``.
+    Global targets: a run sharing the target is one ``global_stage`` exchange.  This is the
     grouping ``sv_apply_gates`` applies natively, exposed so each pass can be
     timed and recorded on its own."""
     gates = list(gates)
