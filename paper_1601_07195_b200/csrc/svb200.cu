@@ -364,7 +364,9 @@ struct TileSeg {
   uint8_t S[4];       // tile bits held in register bits 0..TR-1 (ascending)
   uint8_t tbits[12];  // tile bit of thread-index bit b
   int16_t first, count;
-  int8_t natural, pad[3];
+  int8_t natural;
+  int8_t plain;  // every gate of the segment is uncontrolled and general: the lean gate loop
+  int8_t pad[2];
 };
 
 // A tile is 2^T amplitudes: tile bits 0..T-5 are slice bits 0..T-5 (contiguous
@@ -538,6 +540,20 @@ __device__ __forceinline__ void tile_body(const double2 *__restrict__ a, uint64_
     cbase = base;
 #pragma unroll
     for (int k = 0; k < TR; ++k) c[k] = mm[k];
+#ifndef SV_TILE_NO_PLAIN
+    if (S.plain) {  // one dispatch level (register bit) instead of three: fewer register shuffles
+      for (int gi = S.first; gi < S.first + S.count; ++gi) {
+        const TileGate &G = P.g[gi];
+        switch (G.tb) {
+          case 0: tile_gate_k<0, KIND_GENERAL, true, SPEC>(r, TFULL, G.q); break;
+          case 1: tile_gate_k<1, KIND_GENERAL, true, SPEC>(r, TFULL, G.q); break;
+          case 2: tile_gate_k<2, KIND_GENERAL, true, SPEC>(r, TFULL, G.q); break;
+          default: tile_gate_k<TR - 1, KIND_GENERAL, true, SPEC>(r, TFULL, G.q); break;
+        }
+      }
+      continue;
+    }
+#endif
     for (int gi = S.first; gi < S.first + S.count; ++gi) {
       const TileGate &G = P.g[gi];
       uint32_t pm = TFULL;
@@ -1330,6 +1346,9 @@ int plan_tile(const sv_gate *gates, int n, int T, const int (&hb)[TR], TileParam
       ++gi;
     }
     seg.count = (int16_t)(gi - seg.first);
+    bool plain = true;
+    for (int k = seg.first; k < gi; ++k) plain &= P.g[k].cmode == 0 && P.g[k].kind == KIND_GENERAL;
+    seg.plain = plain ? 1 : 0;
     ++P.nsegs;
   }
   P.last_natural = P.seg[P.nsegs - 1].natural;
