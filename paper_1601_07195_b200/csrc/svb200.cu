@@ -406,11 +406,25 @@ __device__ __forceinline__ int swz(int i) {
   return i ^ (h & 7);
 }
 
-__device__ __forceinline__ int reg_off(int j, const int (&m)[TR]) {
-  int o = 0;
+// swz is linear over GF(2) (shifts, XORs, a constant mask) and the thread part
+// and the register masks occupy disjoint bits, so the slot of register j is
+// swz(base) ^ XOR_{k in j} swz(m[k]).  Visiting the registers in Gray-code order
+// turns the 16 addresses into one XOR each (instead of ~9 ALU ops per address).
+template <bool STORE>
+__device__ __forceinline__ void tile_xfer(double2 *s, double2 (&r)[TRN], int base, const int (&m)[TR]) {
+  int sm[TR];
 #pragma unroll
-  for (int k = 0; k < TR; ++k) o |= ((j >> k) & 1) ? m[k] : 0;
-  return o;
+  for (int k = 0; k < TR; ++k) sm[k] = swz(m[k]);
+  int ad = swz(base);
+#pragma unroll
+  for (int i = 0; i < TRN; ++i) {
+    const int g = i ^ (i >> 1);  // Gray code: g(i) and g(i-1) differ in bit ctz(i)
+    if (i) ad ^= sm[(i & 1) ? 0 : (i & 2) ? 1 : (i & 4) ? 2 : 3];  // ctz(i), i < 16
+    if (STORE)
+      s[ad] = r[g];
+    else
+      r[g] = s[ad];
+  }
 }
 
 // The TRN/2 register pairs of a gate on register bit TB, processed in groups
@@ -530,11 +544,9 @@ __device__ __forceinline__ void tile_body(const double2 *__restrict__ a, uint64_
     for (int b = 0; b < T - TR; ++b) base |= ((tid >> b) & 1) << S.tbits[b];
     if (!(sg == 0 && S.natural)) {
       if (touched) __syncthreads();
-#pragma unroll
-      for (int j = 0; j < TRN; ++j) s[swz(cbase | reg_off(j, c))] = r[j];
+      tile_xfer<true>(s, r, cbase, c);
       __syncthreads();
-#pragma unroll
-      for (int j = 0; j < TRN; ++j) r[j] = s[swz(base | reg_off(j, mm))];
+      tile_xfer<false>(s, r, base, mm);
       touched = true;
     }
     cbase = base;
@@ -573,11 +585,12 @@ __device__ __forceinline__ void tile_body(const double2 *__restrict__ a, uint64_
   }
   if (!P.last_natural) {
     if (touched) __syncthreads();
-#pragma unroll
-    for (int j = 0; j < TRN; ++j) s[swz(cbase | reg_off(j, c))] = r[j];
+    tile_xfer<true>(s, r, cbase, c);
     __syncthreads();
+    int nat[TR];
 #pragma unroll
-    for (int j = 0; j < TRN; ++j) r[j] = s[swz(tid + j * NT)];
+    for (int k = 0; k < TR; ++k) nat[k] = NT << k;
+    tile_xfer<false>(s, r, tid, nat);
   }
 }
 
