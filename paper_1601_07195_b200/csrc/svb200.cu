@@ -390,15 +390,6 @@ __device__ __forceinline__ uint64_t tile_base(uint64_t b, const int (&hb)[TR]) {
   return x;
 }
 
-// slice offset (relative to the tile base) of natural-layout register j of thread tid
-template <int T>
-__device__ __forceinline__ uint64_t tile_off(int tid, int j, const int (&hb)[TR]) {
-  uint64_t o = (uint64_t)tid;
-#pragma unroll
-  for (int k = 0; k < TR; ++k) o |= (uint64_t)((j >> k) & 1) << hb[k];
-  return o;
-}
-
 __device__ __forceinline__ int swz(int i) {
   int h = i >> 3;
   h ^= h >> 3;
@@ -410,6 +401,23 @@ __device__ __forceinline__ int swz(int i) {
 // and the register masks occupy disjoint bits, so the slot of register j is
 // swz(base) ^ XOR_{k in j} swz(m[k]).  Visiting the registers in Gray-code order
 // turns the 16 addresses into one XOR each (instead of ~9 ALU ops per address).
+// Global load / store of a thread's natural-layout registers: the offsets
+// tid | XOR_{k in j} 2^hb[k] (disjoint bits), visited in Gray-code order.
+template <bool STORE>
+__device__ __forceinline__ void tile_gxfer(double2 *__restrict__ a, double2 (&r)[TRN], uint64_t tile0, int tid,
+                                           const int (&hb)[TR]) {
+  uint64_t off = tile0 | (uint64_t)tid;  // tile0 is zero on every tile bit
+#pragma unroll
+  for (int i = 0; i < TRN; ++i) {
+    const int g = i ^ (i >> 1);
+    if (i) off ^= 1ull << hb[(i & 1) ? 0 : (i & 2) ? 1 : (i & 4) ? 2 : 3];
+    if (STORE)
+      a[off] = r[g];
+    else
+      r[g] = a[off];
+  }
+}
+
 template <bool STORE>
 __device__ __forceinline__ void tile_xfer(double2 *s, double2 (&r)[TRN], int base, const int (&m)[TR]) {
   int sm[TR];
@@ -527,8 +535,7 @@ template <int T, bool SPEC>
 __device__ __forceinline__ void tile_body(const double2 *__restrict__ a, uint64_t tile0, const int (&hb)[TR],
                                           int tid, const TileParams &P, double2 *s, double2 (&r)[TRN]) {
   constexpr int NT = 1 << (T - TR);
-#pragma unroll
-  for (int j = 0; j < TRN; ++j) r[j] = a[tile0 + tile_off<T>(tid, j, hb)];
+  tile_gxfer<false>(const_cast<double2 *>(a), r, tile0, tid, hb);
   // current layout: natural (register bits = top TR tile bits, thread bits ascending)
   int cbase = tid, c[TR];
 #pragma unroll
@@ -607,8 +614,7 @@ __device__ __noinline__ void tile_replay(double2 *__restrict__ a, uint64_t tile0
   const int tid = threadIdx.x;
   double2 r[TRN];
   tile_body<T, false>(a, tile0, hb, tid, *P, s, r);
-#pragma unroll
-  for (int j = 0; j < TRN; ++j) a[tile0 + tile_off<T>(tid, j, hb)] = r[j];
+  tile_gxfer<true>(a, r, tile0, tid, hb);
 }
 
 // SPEC = true when the run is mostly diagonal/phase gates (host-chosen):
@@ -638,8 +644,7 @@ __global__ void __launch_bounds__(1 << (T - TR), (T <= 12) ? SV_TILE_MINB : 1)
       return;
     }
   }
-#pragma unroll
-  for (int j = 0; j < TRN; ++j) a[tile0 + tile_off<T>(tid, j, hb)] = r[j];
+  tile_gxfer<true>(a, r, tile0, tid, hb);
 }
 
 // ------------------------------------------------- same-target stages (exchange)
