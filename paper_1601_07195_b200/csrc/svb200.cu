@@ -506,29 +506,6 @@ __device__ __forceinline__ void tile_gate_k(double2 (&r)[TRN], uint32_t pm, cons
   }
 }
 
-template <int TB, bool SPEC>
-__device__ __forceinline__ void tile_gate(double2 (&r)[TRN], uint32_t pm, int kind, const double *q) {
-  if (pm == 0u) return;
-  if (!SPEC && kind >= KIND_REAL) kind = KIND_GENERAL;  // the exact pass runs mix() for them
-  if (pm == TFULL) {  // uncontrolled, or control decided per thread/CTA: straight-line code
-    switch (kind) {
-      case KIND_GENERAL: tile_gate_k<TB, KIND_GENERAL, true, SPEC>(r, pm, q); break;
-      case KIND_PHASE: tile_gate_k<TB, KIND_PHASE, true, SPEC>(r, pm, q); break;
-      case KIND_DIAG: tile_gate_k<TB, KIND_DIAG, true, SPEC>(r, pm, q); break;
-      case KIND_REAL: if (SPEC) tile_gate_k<TB, KIND_REAL, true, SPEC>(r, pm, q); break;
-      default: if (SPEC) tile_gate_k<TB, KIND_HSHARE, true, SPEC>(r, pm, q); break;
-    }
-    return;
-  }
-  switch (kind) {
-    case KIND_GENERAL: tile_gate_k<TB, KIND_GENERAL, false, SPEC>(r, pm, q); break;
-    case KIND_PHASE: tile_gate_k<TB, KIND_PHASE, false, SPEC>(r, pm, q); break;
-    case KIND_DIAG: tile_gate_k<TB, KIND_DIAG, false, SPEC>(r, pm, q); break;
-    case KIND_REAL: if (SPEC) tile_gate_k<TB, KIND_REAL, false, SPEC>(r, pm, q); break;
-    default: if (SPEC) tile_gate_k<TB, KIND_HSHARE, false, SPEC>(r, pm, q); break;
-  }
-}
-
 // One tile through the run: load (natural layout), segments with transposes,
 // back to the natural layout in registers (the caller stores).
 template <int T, bool SPEC>
@@ -582,11 +559,21 @@ __device__ __forceinline__ void tile_body(const double2 *__restrict__ a, uint64_
         pm = ((base >> G.cbit) & 1) ? TFULL : 0u;
       else if (G.cmode == 3)
         pm = ((tile0 >> G.cabove) & 1ull) ? TFULL : 0u;
-      switch (G.tb) {
-        case 0: tile_gate<0, SPEC>(r, pm, G.kind, G.q); break;
-        case 1: tile_gate<1, SPEC>(r, pm, G.kind, G.q); break;
-        case 2: tile_gate<2, SPEC>(r, pm, G.kind, G.q); break;
-        default: tile_gate<TR - 1, SPEC>(r, pm, G.kind, G.q); break;
+      if (pm == 0u) continue;  // control decided per thread / CTA: clear
+      // one flat dispatch on (register bit, kind, all pairs or a register-bit control)
+      const int kind = (!SPEC && G.kind >= KIND_REAL) ? KIND_GENERAL : G.kind;
+      switch ((G.tb * KIND_COUNT + kind) * 2 + (pm != TFULL)) {
+#define TF_CASE(TB_, K_, P_)                                                                       \
+  case ((TB_)*KIND_COUNT + (K_)) * 2 + (P_):                                                      \
+    tile_gate_k<((TB_) < TR ? (TB_) : TR - 1), K_, (P_) == 0, SPEC>(r, pm, G.q);                 \
+    break;
+#define TF_K(TB_, K_) TF_CASE(TB_, K_, 0) TF_CASE(TB_, K_, 1)
+#define TF_TB(TB_) TF_K(TB_, KIND_GENERAL) TF_K(TB_, KIND_DIAG) TF_K(TB_, KIND_PHASE) TF_K(TB_, KIND_REAL) TF_K(TB_, KIND_HSHARE)
+        TF_TB(0) TF_TB(1) TF_TB(2) TF_TB(3)
+#undef TF_TB
+#undef TF_K
+#undef TF_CASE
+        default: break;
       }
     }
   }

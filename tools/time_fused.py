@@ -39,6 +39,11 @@ def main():
     ctl = [c for c in range(n) if c != k][:29]
     stage = [sv.GateOp(sv.hadamard(), k)] + [sv.GateOp(sv.phase_r(j + 2), k, c) for j, c in enumerate(ctl)]
     tile = [sv.GateOp(sv.random_unitary(rng), int(rng.integers(12))) for _ in range(64)]
+    tile_ctl = []
+    for _ in range(64):
+        t = int(rng.integers(12))
+        c = None if rng.random() < 0.5 else int((t + 1 + rng.integers(n - 1)) % n)
+        tile_ctl.append(sv.GateOp(sv.random_unitary(rng), t, c))
     diag = []
     for t in range(12):
         diag.append(sv.GateOp(sv.hadamard(), t))
@@ -49,6 +54,7 @@ def main():
         "n": n,
         "stage30_ms": timed(lambda: sv.kernels.apply_gates(st.amps, stage), reps),
         "tile64_random_ms": timed(lambda: sv.kernels.apply_gates(st.amps, tile, tile=12), reps),
+        "tile64_ctl_ms": timed(lambda: sv.kernels.apply_gates(st.amps, tile_ctl, tile=12), reps),
         "tile_qft12_ms": timed(lambda: sv.kernels.apply_gates(st.amps, diag, tile=12), reps),
         "qft_ms": timed(lambda: sv.run_circuit(st, qft, fusion=fc), reps),
     }
