@@ -44,7 +44,7 @@ extern "C" {
 /* One local stage pass (SV_GROUP_STAGE): at most this many gates, whose targets
  * fall in at most SV_MSTAGE_MAX_TARGETS distinct qubits (controls anywhere). */
 #define SV_MSTAGE_MAX_GATES 128
-#define SV_MSTAGE_MAX_TARGETS 3
+#define SV_MSTAGE_MAX_TARGETS 4
 /* Scratch doubles sv_norm_sq needs (per-block partials + result). */
 #define SV_NORM_SCRATCH 1025
 
@@ -93,7 +93,7 @@ int sv_apply_gates(void *amps, int m, const sv_gate *gates, int ngates, int tile
 /* Launch-group kinds of the pass planner. */
 #define SV_GROUP_GATES 0 /* one launch per gate (sv_apply_single / sv_apply_controlled) */
 #define SV_GROUP_TILE 1  /* register-tiled run: targets < tile-4 plus up to four higher bits */
-#define SV_GROUP_STAGE 2 /* stage: targets in <= SV_MSTAGE_MAX_TARGETS qubits, 8 amplitudes per thread */
+#define SV_GROUP_STAGE 2 /* stage: targets in <= SV_MSTAGE_MAX_TARGETS qubits, 16 amplitudes per thread */
 
 /* The planner of sv_apply_gates, exposed (pure host code, no GPU needed):
  * writes the end index and kind of each launch group, returns the number of

@@ -823,9 +823,9 @@ __device__ __forceinline__ void stage_apply_exact(double2 (&x0)[SUNROLL], double
 
 // ------------------------------------------------------------ multi-target stages
 //
-// A run of gates whose targets lie in at most MS_K = 3 slice bits ("slots"),
-// controls anywhere, in ONE HBM pass: each thread holds the 8 amplitudes that
-// span the three slot bits and applies the whole run in registers -- e.g. three
+// A run of gates whose targets lie in at most MS_K = 4 slice bits ("slots"),
+// controls anywhere, in ONE HBM pass: each thread holds the 16 amplitudes that
+// span the four slot bits and applies the whole run in registers -- e.g. four
 // consecutive transform stages H(k), R(k, c) for all c < k.  A run with fewer
 // targets is padded with the most used control bits, which turns those
 // controls into compile-time pair patterns.
@@ -846,10 +846,23 @@ __device__ __forceinline__ void stage_apply_exact(double2 (&x0)[SUNROLL], double
 // a zero replays its group exactly, out of line (ms_replay).
 
 #ifndef SV_MS_MINB
-#define SV_MS_MINB 4  // CTAs per SM the register budget must allow (measured: 2, 3, 4 -> QFT(30) 149, 120, 95 ms)
+// Threads per SM the register budget must allow, in units of 256.  Measured, QFT(30):
+// 8 amplitudes per thread (MS_K = 3): 2, 3, 4 -> 149, 120, 85 ms; 16 amplitudes (MS_K = 4):
+// 512 / 640 / 768 / 896 threads -> 95 / 80 / 76.6 / 82 ms.  At 768 (80 registers) ptxas keeps
+// ~1 KB per thread in local memory and the kernel is still fastest: it is bound by FP64
+// latency with too few warps, not by the L1 traffic of the spills.
+#define SV_MS_MINB 3
 #endif
-constexpr int MS_K = 3;
+#ifndef SV_MS_K
+#define SV_MS_K SV_MSTAGE_MAX_TARGETS  // slot bits per thread (2^MS_K amplitudes in registers)
+#endif
+constexpr int MS_K = SV_MS_K;
+static_assert(MS_K == 3 || MS_K == 4, "stage slot bits");
 constexpr int MS_N = 1 << MS_K;
+#ifndef SV_MS_BLK
+#define SV_MS_BLK 256  // K = 4, 3 CTAs/SM: 64/256 threads per CTA -> QFT(30) 80.3/76.6 ms (128: 79.1)
+#endif
+constexpr int MS_BLK = SV_MS_BLK;
 constexpr int MS_MAX = SV_MSTAGE_MAX_GATES;
 
 struct MsGate {
@@ -918,8 +931,14 @@ __device__ __forceinline__ void ms_dispatch(int code, double2 (&r)[MS_N], uint32
   case ((K_) * MS_K + (S_)) * (MS_K + 1) + (C_):      \
     ms_loop<S_, C_, K_>(r, act, lane_dep, g0, base, P); \
     break;
+#if SV_MS_K == 3
 #define MS_CASES_S(K_, S_) MS_CASE(K_, S_, 0) MS_CASE(K_, S_, 1) MS_CASE(K_, S_, 2) MS_CASE(K_, S_, 3)
 #define MS_CASES(K_) MS_CASES_S(K_, 0) MS_CASES_S(K_, 1) MS_CASES_S(K_, 2)
+#else
+#define MS_CASES_S(K_, S_) \
+  MS_CASE(K_, S_, 0) MS_CASE(K_, S_, 1) MS_CASE(K_, S_, 2) MS_CASE(K_, S_, 3) MS_CASE(K_, S_, 4)
+#define MS_CASES(K_) MS_CASES_S(K_, 0) MS_CASES_S(K_, 1) MS_CASES_S(K_, 2) MS_CASES_S(K_, 3)
+#endif
     MS_CASES(KIND_GENERAL) MS_CASES(KIND_DIAG) MS_CASES(KIND_PHASE) MS_CASES(KIND_REAL) MS_CASES(KIND_HSHARE)
 #undef MS_CASES
 #undef MS_CASES_S
@@ -928,8 +947,11 @@ __device__ __forceinline__ void ms_dispatch(int code, double2 (&r)[MS_N], uint32
   }
 }
 
-__device__ __forceinline__ uint64_t ms_off(int j, uint64_t b0, uint64_t b1, uint64_t b2) {
-  return ((j & 1) ? b0 : 0ull) | ((j & 2) ? b1 : 0ull) | ((j & 4) ? b2 : 0ull);
+__device__ __forceinline__ uint64_t ms_off(int j, const uint64_t (&b)[MS_K]) {
+  uint64_t o = 0;
+#pragma unroll
+  for (int s = 0; s < MS_K; ++s) o |= ((j >> s) & 1) ? b[s] : 0ull;
+  return o;
 }
 
 // The speculative run (all 32 lanes of the warp take part).
@@ -981,10 +1003,12 @@ __device__ __forceinline__ void ms_exact(double2 (&r)[MS_N], int cs, const doubl
 
 // Exact replay of one thread's group from global memory (nothing stored yet).
 __device__ __noinline__ void ms_replay(double2 *__restrict__ a, uint64_t base, const MsParams *P) {
-  const uint64_t b0 = 1ull << P->bits[0], b1 = 1ull << P->bits[1], b2 = 1ull << P->bits[2];
+  uint64_t b[MS_K];
+#pragma unroll
+  for (int s = 0; s < MS_K; ++s) b[s] = 1ull << P->bits[s];
   double2 r[MS_N];
 #pragma unroll
-  for (int j = 0; j < MS_N; ++j) r[j] = a[base | ms_off(j, b0, b1, b2)];
+  for (int j = 0; j < MS_N; ++j) r[j] = a[base | ms_off(j, b)];
   for (int gi = 0; gi < P->ngates; ++gi) {
     const int c = P->cbit[gi];
     if (c != 0xFF && !((base >> c) & 1ull)) continue;
@@ -994,28 +1018,30 @@ __device__ __noinline__ void ms_replay(double2 *__restrict__ a, uint64_t base, c
       ms_exact<0>(r, cs, P->g[gi].q);
     else if (s == 1)
       ms_exact<1>(r, cs, P->g[gi].q);
-    else
+    else if (MS_K == 3 || s == 2)
       ms_exact<2>(r, cs, P->g[gi].q);
+    else
+      ms_exact<MS_K - 1>(r, cs, P->g[gi].q);
   }
 #pragma unroll
-  for (int j = 0; j < MS_N; ++j) a[base | ms_off(j, b0, b1, b2)] = r[j];
+  for (int j = 0; j < MS_N; ++j) a[base | ms_off(j, b)] = r[j];
 }
 
-#ifndef SV_MS_BLK
-#define SV_MS_BLK 128  // measured 64/128/256/512: QFT(30) 87.9/86.1/87.0/90.1 ms
-#endif
-constexpr int MS_BLK = SV_MS_BLK;
 
 __global__ void __launch_bounds__(MS_BLK, SV_MS_MINB * 256 / MS_BLK) k_mstage(double2 *__restrict__ a,
                                                                           uint64_t ngroups,
                                                                           const __grid_constant__ MsParams P) {
   const uint64_t p = (uint64_t)blockIdx.x * MS_BLK + threadIdx.x;
-  const uint64_t b0 = 1ull << P.bits[0], b1 = 1ull << P.bits[1], b2 = 1ull << P.bits[2];
-  const uint64_t base = insert_zero(insert_zero(insert_zero(p, P.bits[0]), P.bits[1]), P.bits[2]);
+  uint64_t b[MS_K], base = p;
+#pragma unroll
+  for (int s = 0; s < MS_K; ++s) {
+    b[s] = 1ull << P.bits[s];
+    base = insert_zero(base, P.bits[s]);
+  }
   const bool live = p < ngroups;
   double2 r[MS_N];
 #pragma unroll
-  for (int j = 0; j < MS_N; ++j) r[j] = live ? a[base | ms_off(j, b0, b1, b2)] : make_double2(1.0, 1.0);
+  for (int j = 0; j < MS_N; ++j) r[j] = live ? a[base | ms_off(j, b)] : make_double2(1.0, 1.0);
   ms_run(r, base, P);
   bool ok = true;
 #pragma unroll
@@ -1026,7 +1052,7 @@ __global__ void __launch_bounds__(MS_BLK, SV_MS_MINB * 256 / MS_BLK) k_mstage(do
     return;
   }
 #pragma unroll
-  for (int j = 0; j < MS_N; ++j) a[base | ms_off(j, b0, b1, b2)] = r[j];
+  for (int j = 0; j < MS_N; ++j) a[base | ms_off(j, b)] = r[j];
 }
 
 // ---------------------------------------------------------------- half exchange
@@ -1489,7 +1515,7 @@ int run_mstage(double2 *a, int m, const sv_gate *gates, int n, cudaStream_t st) 
 // Native pass planner: the launch group starting at gates[i], returned as its end.
 // Candidate 1, a register-tiled run: targets below L = T-4, or one of up to four
 // higher slice bits taken in order of appearance (the tile then gathers those
-// bits).  Candidate 2, a stage: the run whose targets stay within MS_K = 3
+// bits).  Candidate 2, a stage: the run whose targets stay within MS_K = 4
 // distinct bits.  Cost model (B200, ms at 2^30 amplitudes, compute overlapping
 // HBM): a pass costs max(5, sum of per-gate costs); per gate, tile 1.15
 // general / 0.45 diagonal (real 0.75, Hadamard-like 0.55), stage by structure (general 0.9, real 0.55,

@@ -206,7 +206,7 @@ def launch_fused(amps, ops: list, l: int) -> None:
 def apply_gates(amps, ops, tile: int = 0) -> None:
     """Native pass planner (sv_apply_gates): local gates applied in order, grouped into
     register-tiled runs (targets < tile, controls anywhere) and multi-target stage passes
-    (runs whose targets lie in at most three qubits).
+    (runs whose targets lie in at most four qubits).
     Bit-identical to applying them one by one."""
     ptr, m = device_view(amps)
     ops = list(ops)

@@ -9,8 +9,8 @@ allow, without reordering any gate:
   anywhere; a control in the rank bits turns into "uncontrolled" or "skip" on
   this rank).  Executed by ``sv_apply_gates``: register-tiled runs for
   targets below the tile (2^12) plus up to four gathered higher qubits,
-  multi-target stage passes for runs whose targets lie in at most three qubits
-  (three transform stages H(k), R(k, c) for all c are ONE pass), single-gate
+  multi-target stage passes for runs whose targets lie in at most four qubits
+  (four transform stages H(k), R(k, c) for all c are ONE pass), single-gate
   kernels otherwise -- whichever covers the run more cheaply (svb200.cu
   ``next_group``).
 * ``global_stage`` -- a run of gates sharing one global target: ONE fused

@@ -1,6 +1,6 @@
 """GPU: multi-target stage passes (k_mstage) -- bitwise against the oracle.
 
-One stage launch applies a run of gates whose targets lie in at most three
+One stage launch applies a run of gates whose targets lie in at most four
 qubits; controls anywhere: on a slot bit (compile-time pair pattern), on a lane
 bit (per-lane), above the lanes (warp-uniform ballot), including runs longer
 than 32 gates (several ballot chunks) and the 128-gate maximum.  Every update
@@ -46,7 +46,8 @@ def stage_ops(rng, n, targets, count, cfrac=0.7, controls=None):
 
 
 @pytest.mark.parametrize("n,targets", [(8, [5, 6, 7]), (12, [11, 3, 7]), (14, [0, 1, 2]), (16, [9]),
-                                       (16, [15, 4]), (18, [17, 16, 15]), (20, [8, 0, 19])])
+                                       (16, [15, 4]), (18, [17, 16, 15]), (20, [8, 0, 19]), (10, [6, 7, 8, 9]),
+                                       (16, [0, 1, 2, 3]), (20, [19, 3, 11, 0]), (22, [21, 20, 19, 18])])
 def test_stage_runs_bitwise(n, targets):
     rng = np.random.default_rng(4000 + 31 * n + sum(targets))
     for trial in range(3):
@@ -58,12 +59,13 @@ def test_stage_runs_bitwise(n, targets):
         assert bits_equal(a.cpu().numpy(), run_oracle(v, ops)), (n, targets, trial)
 
 
+@pytest.mark.parametrize("nslots", [3, 4])
 @pytest.mark.parametrize("ctl", ["lanes", "warp", "cta", "slots"])
-def test_stage_control_placements(ctl):
-    """Controls only on lane bits (0..4), warp bits (5..7), CTA bits (>= 11) or the slot bits."""
-    n, targets = 17, [8, 9, 10]
-    pool = {"lanes": range(5), "warp": range(5, 8), "cta": range(11, n), "slots": targets}[ctl]
-    rng = np.random.default_rng({"lanes": 1, "warp": 2, "cta": 3, "slots": 4}[ctl])
+def test_stage_control_placements(ctl, nslots):
+    """Controls only on lane bits (0..4), warp bits (5..7), CTA bits (above the slots) or the slot bits."""
+    n, targets = 17 + nslots - 3, list(range(8, 8 + nslots))
+    pool = {"lanes": range(5), "warp": range(5, 8), "cta": range(8 + nslots, n), "slots": targets}[ctl]
+    rng = np.random.default_rng({"lanes": 1, "warp": 2, "cta": 3, "slots": 4}[ctl] + 10 * nslots)
     v = random_state(rng, n)
     ops = stage_ops(rng, n, targets, 100, cfrac=0.9, controls=list(pool))
     a = torch.from_numpy(v.copy()).to(DEV)
@@ -102,21 +104,24 @@ def test_stage_abi_guards():
     a = torch.zeros(1 << 10, dtype=torch.complex128, device=DEV)
     ptr, m = device_view(a)
     L = _lib.load()
-    four = [sv.GateOp(sv.hadamard(), t) for t in (1, 2, 3, 4)]
-    assert L.sv_apply_group(ptr, m, _lib.SV_GROUP_STAGE, gate_array(four), 4, 0, stream_handle()) == _lib.SV_EINVAL
+    five = [sv.GateOp(sv.hadamard(), t) for t in (1, 2, 3, 4, 5)]
+    assert L.sv_apply_group(ptr, m, _lib.SV_GROUP_STAGE, gate_array(five), 5, 0, stream_handle()) == _lib.SV_EINVAL
     assert "distinct targets" in L.sv_last_error().decode()
+    small = torch.zeros(1 << 3, dtype=torch.complex128, device=DEV)  # fewer bits than slots
+    sptr, sm = device_view(small)
+    assert L.sv_apply_group(sptr, sm, _lib.SV_GROUP_STAGE, gate_array(five[:2]), 2, 0, stream_handle()) == _lib.SV_EINVAL
     many = [sv.GateOp(sv.hadamard(), 1)] * (_lib.SV_MSTAGE_MAX_GATES + 1)
     assert L.sv_apply_group(ptr, m, _lib.SV_GROUP_STAGE, gate_array(many), len(many), 0,
                             stream_handle()) == _lib.SV_EINVAL
 
 
-@pytest.mark.parametrize("n", [3, 4, 5, 6, 7])
+@pytest.mark.parametrize("n", [4, 5, 6, 7, 8])
 def test_stage_tiny_slices_partial_warps(n):
     """Slices with fewer than 32 groups (partial warps take part in the ballots with dummy rows)."""
     rng = np.random.default_rng(600 + n)
     for trial in range(4):
         v = with_zeros(rng, n) if trial % 2 else random_state(rng, n)
-        targets = [int(t) for t in rng.choice(n, min(3, n), replace=False)]
+        targets = [int(t) for t in rng.choice(n, min(_lib.SV_MSTAGE_MAX_TARGETS, n), replace=False)]
         ops = stage_ops(rng, n, targets, [5, 40, 77, 128][trial])
         a = torch.from_numpy(v.copy()).to(DEV)
         apply_stage(a, ops)

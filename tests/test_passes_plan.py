@@ -8,14 +8,16 @@ import paper_1601_07195_b200 as sv
 from paper_1601_07195_b200.passes import _resolve_rank_controls, tile_for
 
 
-def test_qft_plan_is_one_pass_per_three_stages():
+def test_qft_plan_is_one_pass_per_four_stages():
     n, m = 30, 30
     circ = sv.build_qft(n)
     plan = sv.plan_passes(circ.gates, m, 12)
-    # three consecutive transform stages H(k), R(k, c) for all c < k share one stage pass; the
-    # last three (targets 0..2, strided for a stage) go through the register tile
-    assert [p.kind for p in plan] == ["local_stage"] * 9 + ["local_tile"]
-    assert [sorted({op.target for op in p.gates}) for p in plan] == [[k - 2, k - 1, k] for k in range(29, 0, -3)]
+    # four consecutive transform stages H(k), R(k, c) for all c < k share one stage pass; the
+    # last two (targets 0..1, strided for a stage) go through the register tile
+    assert sv._lib.SV_MSTAGE_MAX_TARGETS == 4
+    assert [p.kind for p in plan] == ["local_stage"] * 7 + ["local_tile"]
+    assert [sorted({op.target for op in p.gates}) for p in plan] == (
+        [[k - 3, k - 2, k - 1, k] for k in range(29, 2, -4)] + [[0, 1]])
     assert [op for p in plan for op in p.gates] == list(circ.gates)
     assert max(len(p.gates) for p in plan) <= sv._lib.SV_MSTAGE_MAX_GATES
 
@@ -55,7 +57,7 @@ def test_plan_is_rank_independent_and_tile_bounds():
             if p.kind == "local_tile":  # low bits < T-4 plus at most four gathered high bits
                 assert len({op.target for op in p.gates if op.target >= tile_for(12, m) - 4}) <= 4
             if p.kind == "local_stage":
-                assert len({op.target for op in p.gates}) <= 3 and len(p.gates) > 1
+                assert len({op.target for op in p.gates}) <= sv._lib.SV_MSTAGE_MAX_TARGETS and len(p.gates) > 1
     assert tile_for(5, 30) == 0 and tile_for(20, 30) == 13 and tile_for(12, 11) == 11
 
 
@@ -67,7 +69,7 @@ from hypothesis import strategies as st  # noqa: E402
 @settings(max_examples=60, deadline=None)
 def test_native_planner_invariants(m, seed, tile):
     """sv_plan_gates (the planner sv_apply_gates runs): order-preserving cover, one launch per
-    group, tile groups gather at most four bits above T-4, stages span at most three targets."""
+    group, tile groups gather at most four bits above T-4, stages span at most four targets."""
     rng = np.random.default_rng(seed)
     T = tile if tile and tile <= min(m, 13) else min(m, 13)
     zoo = [sv.hadamard(), sv.phase_r(3), sv.pauli_z(), sv.random_unitary(rng)]
