@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--data-plane", choices=["ipc", "nccl"], default="ipc",
                     help="global-qubit exchanges: fused kernel on CUDA-IPC-mapped peer slices (default) or the "
                          "reference's staged pipeline over NCCL send/recv (baseline)")
+    ap.add_argument("--diagonal-local", action="store_true",
+                    help="diagonal gates on global qubits without an exchange (SURVEY.md 8(f)1; off by default: "
+                         "it departs from the reference's per-gate NVLink traffic contract)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
@@ -306,6 +309,8 @@ def make_units(sv, circ, m, fusion, l_c, state, fabric):
             kind, nbytes = "single", 32 << m
         elif case is sv.BoundCase.CONTROLLED_LOCAL:
             kind, nbytes = "controlled", 16 << m
+        elif fabric is not None and fabric.diag_mode and sv.is_diagonal(op.gate):
+            kind, nbytes = "diag-global", 32 << m  # sv_diag_global: one local pass, no exchange
         else:
             kind, nbytes = "exchange", sv.link_bytes_per_direction(case, m)
         units.append((kind, nbytes, 1, (lambda op=op: sv.apply_op(state, op, fabric)), (op,)))
@@ -345,7 +350,7 @@ def main():
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=dev)
-        fabric = sv.NvlinkFabric(data_plane=args.data_plane)
+        fabric = sv.NvlinkFabric(data_plane=args.data_plane, diagonal_local=args.diagonal_local)
     if world & (world - 1):
         raise SystemExit("--gpus must be a power of two")
     g = world.bit_length() - 1
@@ -533,6 +538,7 @@ def main():
                        "n_qubits": n, "local_qubits": m, "global_qubits": g, "gates_per_step": len(timed[0]),
                        "state_gib_per_gpu": (16 << m) / 2**30, "parallelism": f"state sharded over {world} GPU(s)",
                        "data_plane": fabric.data_plane if fabric is not None else None,
+                       "diagonal_local": bool(fabric is not None and fabric.diag_mode),
                        "l2": "no flush: slice >> 126 MB L2" if m >= 26 else "slice fits L2 (parity-size run)",
                        "seed": {"state": 0, "circuit": 1}},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "self_check": self_check,

@@ -137,6 +137,25 @@ int sv_exchange_stage(void *mine, void *theirs, int m, int own_is_zero, const sv
 int sv_exchange(void *mine, void *theirs, int m, int own_is_zero, int c_local, const double *q,
                 void *stream);
 
+/* Diagonal gate (q12 = q21 = 0 exactly) on a global qubit without an exchange
+ * (replaces, behind NvlinkFabric(diagonal_local=True), the
+ * exchange of distributed.py:314-422 for such gates).  Two launches per rank
+ * with a partner fence between them:
+ *   sv_diag_global -- own elements (those with local bit c_local set, or all
+ *     for c_local = -1) *= q11 (zero side) or q22 (one side), in place; writes
+ *     the sign map of the ORIGINAL elements into `signs` (2 bits per element:
+ *     SV_DIAG_SIGN_BYTES(m) bytes) and sets *flag (device int) when a product
+ *     has a zero component;
+ *   sv_diag_fix -- if *flag: for those elements adds the signed-zero partner
+ *     term q12 * partner (q21 on the one side) using the partner's sign map
+ *     (`partner_signs`, its CUDA-IPC mapping), which makes the result equal the
+ *     exchange's mix() bit for bit, sign of zero included. */
+#define SV_DIAG_SIGN_BYTES(m) ((((uint64_t)1 << (m)) + 31) / 32 * 8)
+int sv_diag_global(void *amps, int m, int own_is_zero, int c_local, const double *q, void *signs, int *flag,
+                   void *stream);
+int sv_diag_fix(void *amps, int m, int own_is_zero, int c_local, const double *q, const void *partner_signs,
+                const int *flag, void *stream);
+
 /* Sum of |a|^2 over the slice (qubit = -1) or over local bit `qubit` = 1
  * (core.py:147-167 partials).  Deterministic: fixed grid, fixed reduction
  * order.  `scratch` is a device buffer of SV_NORM_SCRATCH doubles; the result

@@ -59,6 +59,7 @@ from .distributed import (
     gather_full_state,
     make_exchange_plan,
     plan_gate,
+    is_diagonal,
 )
 from .engine import CircuitGraph, GateRecord, run_circuit, run_pipelined
 from .passes import Pass, execute_pass, plan_passes

@@ -28,7 +28,7 @@ EXPORTS = (
     "sv_version", "sv_last_error", "sv_launch_count", "sv_apply_single", "sv_apply_controlled",
     "sv_apply_fused", "sv_apply_gates", "sv_plan_gates", "sv_apply_group", "sv_exchange", "sv_exchange_chunk",
     "sv_exchange_stage", "sv_norm_sq", "sv_init_random", "sv_scale", "sv_init_basis",
-    "sv_copy", "sv_ipc_handle", "sv_ipc_open", "sv_ipc_close",
+    "sv_copy", "sv_ipc_handle", "sv_ipc_open", "sv_ipc_close", "sv_diag_global", "sv_diag_fix",
 )
 
 
@@ -80,6 +80,8 @@ def load() -> ctypes.CDLL:
         "sv_ipc_handle": ([vp, vp, ctypes.POINTER(u64)], i),
         "sv_ipc_open": ([vp, u64, ctypes.POINTER(vp)], i),
         "sv_ipc_close": ([vp, u64], i),
+        "sv_diag_global": ([vp, i, i, i, dp, vp, vp, vp], i),
+        "sv_diag_fix": ([vp, i, i, i, dp, vp, vp, vp], i),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -106,6 +108,11 @@ def qbuf(mat) -> ctypes.Array:
 
     flat = np.ascontiguousarray(np.asarray(mat, dtype=np.complex128).reshape(4)).view(np.float64)
     return (ctypes.c_double * 8)(*flat.tolist())
+
+
+def diag_sign_bytes(m: int) -> int:
+    """SV_DIAG_SIGN_BYTES(m): sign map of sv_diag_global (2 bits per element, 8 bytes per 32)."""
+    return ((1 << m) + 31) // 32 * 8
 
 
 def launch_count() -> int:

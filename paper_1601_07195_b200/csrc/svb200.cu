@@ -1055,6 +1055,67 @@ __global__ void __launch_bounds__(MS_BLK, SV_MS_MINB * 256 / MS_BLK) k_mstage(do
   for (int j = 0; j < MS_N; ++j) a[base | ms_off(j, b)] = r[j];
 }
 
+// ------------------------------------------------ diagonal gates on a global qubit
+//
+// a diagonal gate (q12 = q21 = 0 exactly) on a global target
+// needs no exchange -- the reference's pair update new0 = q11*a0 + q12*a1
+// (distributed.py:187-202, mix() of kernels.py:120-124) is P = cmul(d, own)
+// plus S = cmul(z, partner) with z a signed-zero matrix entry, and S is a
+// signed zero: x + S == x for x != 0.  So each rank multiplies its own
+// elements in place (P), and only where P has a zero component does the exact
+// result depend on the partner -- through the SIGN BITS of the partner's
+// original element alone.  k_diag_global therefore also writes a 2-bit-per-
+// element sign map of its original elements (1/64 of the slice) and raises a
+// flag when any P has a zero component; after a fence, k_diag_fix (a no-op
+// unless the flag is up) re-forms P + S for exactly those elements from the
+// partner's sign map, read through its CUDA-IPC mapping.  Bit-identical to
+// the exchange, zero signs included; non-finite partner amplitudes (outside
+// the normalised-state contract) are not propagated.
+// Sign map layout: two 32-bit words per 32 consecutive elements, bit l of word
+// 2w (2w+1) = sign of element 32w+l's real (imaginary) part.
+
+__global__ void __launch_bounds__(BLK) k_diag_global(double2 *__restrict__ a, uint64_t n, int c, double dr,
+                                                     double di, uint32_t *__restrict__ signs, int *flag) {
+  const uint64_t stride = (uint64_t)gridDim.x * BLK;
+  const uint64_t npad = (n + 31) & ~31ull;
+  bool zero = false;
+  for (uint64_t i = (uint64_t)blockIdx.x * BLK + threadIdx.x; i < npad; i += stride) {
+    const bool act = i < n && (c < 0 || ((i >> c) & 1ull));
+    double2 x = make_double2(0.0, 0.0);
+    if (act) x = a[i];
+    const uint32_t sre = __ballot_sync(0xffffffffu, act && signbit(x.x));
+    const uint32_t sim = __ballot_sync(0xffffffffu, act && signbit(x.y));
+    if ((threadIdx.x & 31) == 0 && (c < 5 || ((i >> c) & 1ull))) {
+      signs[2 * (i >> 5)] = sre;
+      signs[2 * (i >> 5) + 1] = sim;
+    }
+    if (act) {
+      const double2 pv = cmul(dr, di, x);
+      zero |= !nonzero2(pv);
+      a[i] = pv;
+    }
+  }
+  if (__syncthreads_or(zero) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
+__global__ void __launch_bounds__(BLK) k_diag_fix(double2 *__restrict__ a, uint64_t n, int c, double zr, double zi,
+                                                  const uint32_t *__restrict__ psigns, const int *flag) {
+  if (*(volatile const int *)flag == 0) return;
+  const uint64_t stride = (uint64_t)gridDim.x * BLK;
+  for (uint64_t i = (uint64_t)blockIdx.x * BLK + threadIdx.x; i < n; i += stride) {
+    if (c >= 0 && !((i >> c) & 1ull)) continue;
+    const double2 pv = a[i];
+    if (nonzero2(pv)) continue;  // P + (+-0) == P: already exact
+    const uint32_t l = (uint32_t)(i & 31);
+    const uint32_t wre = psigns[2 * (i >> 5)], wim = psigns[2 * (i >> 5) + 1];
+    // cmul(z, w) with z a signed zero depends on w only through its sign bits: +-1 stands in for w
+    const double2 w = make_double2(((wre >> l) & 1u) ? -1.0 : 1.0, ((wim >> l) & 1u) ? -1.0 : 1.0);
+    const double2 sv = cmul(zr, zi, w);
+    a[i] = make_double2(__dadd_rn(pv.x, sv.x), __dadd_rn(pv.y, sv.y));
+  }
+}
+
+
 // ---------------------------------------------------------------- half exchange
 //
 // One rank's side of the pairwise exchange, transfer fused with the update:
@@ -1802,6 +1863,39 @@ int sv_exchange(void *mine, void *theirs, int m, int own_is_zero, int c_local, c
   k_exchange<<<grid_for(count, BLK * UNROLL), BLK, 0, (cudaStream_t)stream>>>(
       (double2 *)mine, (double2 *)theirs, count, base, cmap, own_is_zero ? 1 : 0, load_q(q));
   return after_launch("sv_exchange");
+}
+
+int diag_check(const char *who, void *amps, int m, int c_local, const double *q) {
+  if (bad_ptr(amps) || !q) return fail(SV_EINVAL, "%s: null or misaligned pointer", who);
+  if (m < 1 || m > 62) return fail(SV_EINVAL, "%s: m=%d out of range", who, m);
+  if (c_local < -1 || c_local >= m) return fail(SV_EINVAL, "%s: control %d not local (m=%d)", who, c_local, m);
+  if (!(q[2] == 0.0 && q[3] == 0.0 && q[4] == 0.0 && q[5] == 0.0))
+    return fail(SV_EINVAL, "%s: gate is not diagonal (q12 and q21 must be exactly zero)", who);
+  return SV_OK;
+}
+
+int sv_diag_global(void *amps, int m, int own_is_zero, int c_local, const double *q, void *signs, int *flag,
+                   void *stream) {
+  int rc = diag_check("sv_diag_global", amps, m, c_local, q);
+  if (rc != SV_OK) return rc;
+  if (!signs || !flag) return fail(SV_EINVAL, "sv_diag_global: null sign map or flag");
+  cudaError_t e = cudaMemsetAsync(flag, 0, sizeof(int), (cudaStream_t)stream);
+  if (e != cudaSuccess) return fail(SV_ECUDA, "sv_diag_global: %s", cudaGetErrorString(e));
+  const double dr = own_is_zero ? q[0] : q[6], di = own_is_zero ? q[1] : q[7];
+  k_diag_global<<<fill_grid(1ull << m), BLK, 0, (cudaStream_t)stream>>>((double2 *)amps, 1ull << m, c_local, dr, di,
+                                                                        (uint32_t *)signs, flag);
+  return after_launch("sv_diag_global");
+}
+
+int sv_diag_fix(void *amps, int m, int own_is_zero, int c_local, const double *q, const void *partner_signs,
+                const int *flag, void *stream) {
+  int rc = diag_check("sv_diag_fix", amps, m, c_local, q);
+  if (rc != SV_OK) return rc;
+  if (!partner_signs || !flag) return fail(SV_EINVAL, "sv_diag_fix: null sign map or flag");
+  const double zr = own_is_zero ? q[2] : q[4], zi = own_is_zero ? q[3] : q[5];
+  k_diag_fix<<<fill_grid(1ull << m), BLK, 0, (cudaStream_t)stream>>>((double2 *)amps, 1ull << m, c_local, zr, zi,
+                                                                     (const uint32_t *)partner_signs, flag);
+  return after_launch("sv_diag_fix");
 }
 
 int sv_exchange_chunk(void *mine, void *buf, int m, int own_is_zero, int c_local, const double *q, uint64_t j0,

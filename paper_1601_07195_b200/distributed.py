@@ -144,7 +144,7 @@ class ScratchPool:
 class GateAction:
     """What one rank does for one gate (pure function of layout and gate)."""
 
-    kind: str            # "single" | "controlled" | "exchange" | "idle" (local no-op) | "idle_exchange"
+    kind: str            # "single" | "controlled" | "exchange" | "diag" | "idle" (local no-op) | "idle_exchange"
     case: BoundCase
     target: int
     control: int | None
@@ -157,13 +157,24 @@ class GateAction:
     @property
     def fenced(self) -> bool:
         """Every rank fences around cases 2/5/6 (participating or not)."""
-        return self.kind in ("exchange", "idle_exchange")
+        return self.kind in ("exchange", "diag", "idle_exchange")
 
 
-def plan_gate(layout, target: int, control: int | None) -> GateAction:
-    """Per-rank routing of distributed.py:314-459 (cases of perfmodel.py:30-38)."""
+def plan_gate(layout, target: int, control: int | None, diag: bool = False) -> GateAction:
+    """Per-rank routing of distributed.py:314-459 (cases of perfmodel.py:30-38).
+
+    diag=True (a diagonal gate under NvlinkFabric(diagonal_local=True)):
+    the exchange of cases 2/5/6 becomes a local "diag" action that moves no payload."""
     m, rank = layout.m, layout.rank
     case = classify_case(target, control, m)
+    action = _plan_gate(layout, target, control, m, rank, case)
+    if diag and action.kind == "exchange":
+        return GateAction("diag", case, action.target, action.control, partner=action.partner,
+                          own_is_zero=action.own_is_zero, c_local=action.c_local)
+    return action
+
+
+def _plan_gate(layout, target, control, m, rank, case) -> GateAction:
     if control is None:
         if target < m:
             return GateAction("single", case, target, None)
@@ -271,6 +282,33 @@ class CudaExecutor:
         with torch.cuda.device(state.amps.device):
             _lib.check(_lib.load().sv_copy(dst, src, nbytes, stream_handle()))
 
+    # --- diagonal global gates
+    def diag_alloc(self, state: LocalState):
+        """(sign map, flag) device buffers of sv_diag_global for this slice."""
+        dev = state.amps.device
+        return (torch.empty(_lib.diag_sign_bytes(state.layout.m), dtype=torch.uint8, device=dev),
+                torch.zeros(1, dtype=torch.int32, device=dev))
+
+    def share_buffer(self, state: LocalState, buf):
+        h = (ctypes.c_char * 64)()
+        off = ctypes.c_uint64(0)
+        with torch.cuda.device(state.amps.device):
+            _lib.check(_lib.load().sv_ipc_handle(buf.data_ptr(), h, ctypes.byref(off)))
+        return bytes(h), int(off.value)
+
+    def diag_global(self, state: LocalState, own_is_zero: bool, c_local: int, q: GateMatrix, signs, flag) -> None:
+        ptr, m = device_view(state.amps)
+        with torch.cuda.device(state.amps.device):
+            _lib.check(_lib.load().sv_diag_global(ptr, m, int(own_is_zero), int(c_local), _as_gate(q).qbuf(),
+                                                  signs.data_ptr(), flag.data_ptr(), stream_handle()))
+
+    def diag_fix(self, state: LocalState, own_is_zero: bool, c_local: int, q: GateMatrix, peer_signs: int,
+                 flag) -> None:
+        ptr, m = device_view(state.amps)
+        with torch.cuda.device(state.amps.device):
+            _lib.check(_lib.load().sv_diag_fix(ptr, m, int(own_is_zero), int(c_local), _as_gate(q).qbuf(),
+                                               peer_signs, flag.data_ptr(), stream_handle()))
+
 
 _CUDA = CudaExecutor()
 
@@ -284,7 +322,7 @@ class NvlinkFabric:
     """
 
     def __init__(self, group=None, *, fence: str | None = None, executor=None, data_plane: str = "ipc",
-                 chunk_amps: int = 1 << 26):
+                 chunk_amps: int = 1 << 26, diagonal_local: bool = False):
         import torch.distributed as dist
 
         if not dist.is_initialized():
@@ -313,6 +351,16 @@ class NvlinkFabric:
         self._lock = threading.Lock()
         self._peers: dict[tuple, tuple[list, list]] = {}
         self._flag: torch.Tensor | None = None
+        # SURVEY.md 8(f)1, off by default (it departs from the reference's per-gate traffic
+        # contract, test_acceptance.py:61-71): diagonal gates on global qubits run without an
+        # exchange.  Must be the same on every rank.
+        self.diagonal_local = bool(diagonal_local)
+        self._diag: dict[tuple, tuple] = {}
+
+    @property
+    def diag_mode(self) -> bool:
+        """Diagonal global gates take the no-exchange path (needs peer mappings)."""
+        return self.diagonal_local and self.data_plane == "ipc"
 
     # --- Transport-compatible surface
     def fresh_tag(self) -> int:
@@ -383,10 +431,22 @@ class NvlinkFabric:
                     except Exception as exc:  # noqa: BLE001
                         err = exc
                         break
+        diag = None
+        if err is None and self.diagonal_local:
+            try:
+                diag = self._register_signs(state, ptrs)
+            except Exception as exc:  # noqa: BLE001
+                err = exc
         ok = self.exchange_objects(err is None)
         if all(ok):
             self._peers[key] = (ptrs, blobs)
+            if diag is not None:
+                self._diag[key] = diag
             return
+        if diag is not None:
+            for r, p in enumerate(diag[2]):
+                if p is not None:
+                    self.executor.close(p, diag[3][r])
         for r, p in enumerate(ptrs):
             if p is not None:
                 self.executor.close(p, blobs[r])
@@ -394,6 +454,26 @@ class NvlinkFabric:
 
         warnings.warn(f"peer mapping refused on some rank ({err!r} here); exchanges fall back to NCCL send/recv")
         self.data_plane = "nccl"
+
+    def _register_signs(self, state: LocalState, ptrs) -> tuple:
+        """Sign map + flag of this slice, and every peer's sign map mapped here (collective)."""
+        signs, flag = self.executor.diag_alloc(state)
+        blobs = self.exchange_objects(self.executor.share_buffer(state, signs))
+        peers = [None if r == self.rank else self.executor.open(state, b) for r, b in enumerate(blobs)]
+        return signs, flag, peers, blobs
+
+    def diag_buffers(self, state: LocalState):
+        try:
+            signs, flag, _, _ = self._diag[self.executor.key(state)]
+        except KeyError as exc:
+            raise TransportError("slice not registered for diagonal global gates") from exc
+        return signs, flag
+
+    def peer_signs(self, state: LocalState, rank: int) -> int:
+        try:
+            return self._diag[self.executor.key(state)][2][rank]
+        except (KeyError, IndexError) as exc:
+            raise TransportError("peer sign map not registered") from exc
 
     def nccl_exchange(self, state: LocalState, action: GateAction, q: GateMatrix) -> int:
         """The reference's half exchange over send/recv (distributed.py:205-311), staged in
@@ -458,13 +538,27 @@ class NvlinkFabric:
 
     def release(self, state: LocalState) -> None:
         """Unmap the peers' slices registered for `state` (collective-free)."""
-        entry = self._peers.pop(self.executor.key(state), None)
+        key = self.executor.key(state)
+        entry = self._peers.pop(key, None)
         if entry:
             for ptr, blob in zip(*entry):
                 if ptr is not None:
                     self.executor.close(ptr, blob)
+        diag = self._diag.pop(key, None)
+        if diag:
+            for ptr, blob in zip(diag[2], diag[3]):
+                if ptr is not None:
+                    self.executor.close(ptr, blob)
 
     def close(self) -> None:
+        for key in list(self._diag):
+            _, _, ptrs, blobs = self._diag.pop(key)
+            for ptr, blob in zip(ptrs, blobs):
+                if ptr is not None:
+                    try:
+                        self.executor.close(ptr, blob)
+                    except Exception:
+                        pass
         for key in list(self._peers):
             ptrs, blobs = self._peers.pop(key)
             for ptr, blob in zip(ptrs, blobs):
@@ -487,6 +581,9 @@ def execute_action(state: LocalState, action: GateAction, q: GateMatrix, fabric:
         return
     if fabric is None:
         raise LayoutError(f"gate on qubit {action.target} needs a transport")
+    if action.kind == "diag":
+        _execute_diag(state, action, q, fabric, ex)
+        return
     try:
         # Partner slices are read and written in place: every rank's prior
         # work must be complete before, and the exchange complete after.
@@ -503,6 +600,30 @@ def execute_action(state: LocalState, action: GateAction, q: GateMatrix, fabric:
     except BaseException:
         state.corrupt = True
         raise
+
+
+def _execute_diag(state, action, q, fabric, ex) -> None:
+    """Diagonal gate on a global qubit without an exchange (sv_diag_global / sv_diag_fix):
+    own elements multiplied in place, then -- after a fence, so the partner's sign map of
+    its original elements is complete -- zero components patched from that map.  The
+    trailing fence keeps the next diagonal gate from overwriting a map the partner still
+    reads.  Idle ranks (case 6, control bit clear) take two fences either way."""
+    try:
+        signs, flag = fabric.diag_buffers(state)
+        ex.diag_global(state, action.own_is_zero, action.c_local, q, signs, flag)
+        fabric.barrier(state)
+        ex.diag_fix(state, action.own_is_zero, action.c_local, q, fabric.peer_signs(state, action.partner), flag)
+        fabric.count(0, 0)
+        fabric.barrier(state)
+    except BaseException:
+        state.corrupt = True
+        raise
+
+
+def is_diagonal(q) -> bool:
+    """q12 == q21 == 0 exactly (either zero sign): the diagonal fast path applies."""
+    mat = _as_gate(q).mat
+    return mat[0, 1] == 0 and mat[1, 0] == 0
 
 
 # ------------------------------------------------------------- reference API
@@ -561,12 +682,13 @@ def apply_global(state, target: int, control: int | None, q, transport, *, plan:
     lay = state.layout
     _check_transport(transport, lay)
     transport.fresh_tag()
-    action = plan_gate(lay, target, control)
+    transport.ensure_registered(state)  # collective; may switch every rank to the NCCL data plane
+    diag = getattr(transport, "diag_mode", False) and is_diagonal(q)
+    action = plan_gate(lay, target, control, diag=diag)
     if plan is not None and action.kind == "exchange" and (
             plan.partner != action.partner
             or (plan.this_rank_computes is ComputesHalf.FIRST_HALF) != action.own_is_zero):
         raise TransportError("exchange plan does not match this rank's pairing")
-    transport.ensure_registered(state)
     execute_action(state, action, _as_gate(q), transport, executor)
 
 

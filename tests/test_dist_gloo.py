@@ -83,6 +83,41 @@ class ShmOracleExecutor:
     def synchronize(self, state):
         pass
 
+    # diagonal global gates: the "sign map" stand-in is a shm snapshot of the original slice;
+    # diag_fix forms the reference's mix() from it (the protocol under test: registration,
+    # fences, partner map reads -- the split arithmetic itself is covered on the GPU)
+    def diag_alloc(self, state):
+        shm = shared_memory.SharedMemory(create=True, size=16 << state.layout.m,
+                                         name=f"svd_{os.getpid()}_{state.layout.rank}")
+        self._own = getattr(self, "_own", []) + [shm]
+        return ShmState(state.layout, np.ndarray((1 << state.layout.m,), dtype=np.complex128, buffer=shm.buf),
+                        shm), None
+
+    def share_buffer(self, state, buf):
+        return (buf.shm.name, 0)
+
+    def diag_global(self, state, own_is_zero, c_local, q, signs, flag):
+        signs.amps[:] = state.amps
+
+    def diag_fix(self, state, own_is_zero, c_local, q, peer, flag):
+        m = state.layout.m
+        w = np.frombuffer((ctypes.c_char * (16 << m)).from_address(peer), dtype=np.complex128)
+        x = state.amps
+        sel = slice(None) if c_local < 0 else ((np.arange(1 << m) >> c_local) & 1).astype(bool)
+        mat = q.mat
+        if own_is_zero:
+            out = mat[0, 0] * x[sel]
+            out += mat[0, 1] * w[sel]
+        else:
+            out = mat[1, 0] * w[sel]
+            out += mat[1, 1] * x[sel]
+        x[sel] = out
+
+    def cleanup(self):
+        for shm in getattr(self, "_own", []):
+            shm.close()
+            shm.unlink()
+
     def key(self, state):
         return state.shm.name
 
@@ -272,3 +307,89 @@ def test_gloo_pass_fusion_matches_oracle(world, n):
     m = n - (world.bit_length() - 1)
     stages = [p for p in sv.plan_passes(circ.gates, m) if p.kind == "global_stage"]
     assert len(stages) >= world.bit_length() - 1  # one exchange per global transform stage
+
+
+def _worker_diag(rank, world, port, path, n):
+    """NvlinkFabric(diagonal_local=True): diagonal global gates without an exchange."""
+    import torch.distributed as dist
+
+    import paper_1601_07195_b200 as sv
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        p = world.bit_length() - 1
+        d = dict(np.load(path + ".npz"))
+        lay = sv.Layout(n, p, rank)
+        m = lay.m
+        shm = shared_memory.SharedMemory(create=True, size=16 << m, name=f"svg_{os.getpid()}_{rank}")
+        amps = np.ndarray((1 << m,), dtype=np.complex128, buffer=shm.buf)
+        amps[:] = d["init"][rank << m:(rank + 1) << m]
+        state = ShmState(lay, amps, shm)
+        ex = ShmOracleExecutor()
+        fabric = sv.NvlinkFabric(fence="host", executor=ex, diagonal_local=True)
+        kinds = []
+        for t, c, q in zip(d["t"], d["c"], d["q"]):
+            t, c, gate = int(t), None if c < 0 else int(c), sv.GateMatrix.unchecked(q.reshape(2, 2))
+            if max(t, -1 if c is None else c) < m:
+                (ex.single(state, t, gate) if c is None else ex.controlled(state, c, t, gate))
+            else:
+                kinds.append(sv.plan_gate(lay, t, c, diag=sv.is_diagonal(gate)).kind)
+                sv.apply_global(state, t, c, gate, fabric)
+        fabric.barrier()
+        pids = fabric.exchange_objects(os.getpid())
+        if rank == 0:
+            parts = [amps.copy()]
+            for r in range(1, world):
+                other = shared_memory.SharedMemory(name=f"svg_{pids[r]}_{r}")
+                parts.append(np.ndarray((1 << m,), dtype=np.complex128, buffer=other.buf).copy())
+                other.close()
+            np.savez(path + ".out.npz", full=np.concatenate(parts), sent=fabric.sent_bytes,
+                     ndiag=kinds.count("diag"), fences=fabric.fences)
+        fabric.barrier()
+        fabric.close()
+        ex.cleanup()
+        del amps
+        shm.close()
+        shm.unlink()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n", [(2, 8), (4, 9), (8, 10)])
+def test_gloo_diagonal_local_protocol(world, n):
+    """QFT + diagonal gates on global targets (cases 2, 5, 6) with diagonal_local=True: same state
+    as the oracle; diagonal exchanges move no payload; every rank fences twice per global gate."""
+    import torch.multiprocessing as mp
+
+    import paper_1601_07195_b200 as sv
+    from conftest import random_state
+    from oracle import oracle
+
+    p = world.bit_length() - 1
+    m = n - p
+    rng = np.random.default_rng(world * 7 + n)
+    ops = list(sv.build_qft(n).gates)
+    for k in range(6):
+        q = sv.phase_r(k + 2) if k % 2 else sv.rotation_z(rng.uniform(0, 6))
+        t = m + int(rng.integers(p))
+        for c in [None, 0, m - 1] + [g for g in range(m, n) if g != t][:1]:
+            ops.append(sv.GateOp(q, t, c))
+    ops.append(sv.GateOp(sv.random_unitary(rng), n - 1))
+    init = random_state(rng, n)
+    want = init.copy()
+    oracle.run_circuit(want, ops)
+    with tempfile.TemporaryDirectory() as tmp:
+        path = os.path.join(tmp, "g")
+        np.savez(path + ".npz", init=init, t=np.array([o.target for o in ops]),
+                 c=np.array([-1 if o.control is None else o.control for o in ops]),
+                 q=np.stack([o.gate.mat.reshape(4) for o in ops]))
+        mp.spawn(_worker_diag, args=(world, _port(), path, n), nprocs=world, join=True)
+        out = dict(np.load(path + ".out.npz"))
+    assert np.array_equal(out["full"], want)
+    glob = [o for o in ops if max(o.target, -1 if o.control is None else o.control) >= m]
+    exch = [o for o in glob if o.target >= m and not sv.is_diagonal(o.gate)]
+    assert int(out["ndiag"]) > 0
+    # payload only for the non-diagonal exchanges (H stages of the QFT, the Haar gate): rank 0 takes part
+    # in every uncontrolled one; none for the diagonal ones
+    assert int(out["sent"]) <= sum(1 << (m + 4) for _ in exch)
+    assert int(out["fences"]) == 2 * sum(1 for o in glob if o.target >= m) + 1
