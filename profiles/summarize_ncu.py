@@ -49,6 +49,12 @@ def raw_metrics(rep: str) -> list[dict]:
                     continue
                 d[m] = v * SCALE.get(units[i], 1)
                 d[m + ".unit"] = units[i]
+        stalls = {h[len("smsp__pcsamp_warps_issue_stalled_"):]: float(vals[i].replace(",", "") or 0)
+                  for i, h in enumerate(hdr)
+                  if h.startswith("smsp__pcsamp_warps_issue_stalled_") and not h.endswith("_not_issued")}
+        tot = sum(stalls.values())
+        if tot:
+            d["stalls"] = {k: round(v / tot, 3) for k, v in sorted(stalls.items(), key=lambda x: -x[1])[:6]}
         res.append(d)
     return res
 
@@ -91,6 +97,9 @@ def main():
             for m in METRICS:
                 if m in d:
                     md.append(f"| {m} | {d[m]:.6g} |")
+            if "stalls" in d:
+                md.append("| top warp stall reasons (share of PC samples) | " +
+                          ", ".join(f"{k} {v:.2f}" for k, v in d["stalls"].items()) + " |")
             md += [f"| dram bytes (read+write) | {rd + wr:.6g} |",
                    f"| dram GB/s (ncu, serialised replay) | {(rd + wr) / t / 1e9 if t else 0:.1f} |", ""]
             if i == 0:
