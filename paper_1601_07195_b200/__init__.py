@@ -49,6 +49,7 @@ from .distributed import (
     CudaExecutor,
     ExchangePlan,
     GateAction,
+    InprocFabric,
     NvlinkFabric,
     ScratchPool,
     apply_controlled_distributed,
@@ -61,7 +62,8 @@ from .distributed import (
     plan_gate,
     is_diagonal,
 )
-from .engine import CircuitGraph, GateRecord, run_circuit, run_pipelined
+from .circuitfile import parse_circuit_file, parse_circuit_text
+from .engine import CircuitGraph, GateRecord, run_circuit, run_circuit_inproc, run_pipelined
 from .passes import Pass, execute_pass, plan_passes
 from .errors import CircuitParseError, FusionContractError, LayoutError, ResourceError, TransportError
 from .fusion import (

@@ -569,6 +569,61 @@ class NvlinkFabric:
                         pass
 
 
+class InprocFabric:
+    """Every rank of a layout in ONE process on one device -- the reference's inproc
+    transport (transport.py, driven by cli.py:266-288) without threads.  Rank r's slice is
+    ``states[r]``; a peer mapping is the plain device pointer of the partner's slice, and
+    the caller runs each gate rank by rank on one stream (engine.run_circuit_inproc), so
+    stream order is the fence.  Same exchange kernels, same counters as NvlinkFabric."""
+
+    data_plane = "ipc"
+    diagonal_local = False
+    diag_mode = False
+
+    def __init__(self, states, rank: int):
+        self.states, self.rank, self.num_ranks = states, rank, len(states)
+        self.executor = _CUDA
+        self.sent_bytes = self.received_bytes = 0
+        self.fences = 0
+        self._tag = CONTROL_TAG
+
+    @classmethod
+    def group(cls, states) -> list["InprocFabric"]:
+        return [cls(states, r) for r in range(len(states))]
+
+    def fresh_tag(self) -> int:
+        self._tag += 1
+        return self._tag
+
+    def snapshot(self) -> tuple[int, int]:
+        return self.sent_bytes, self.received_bytes
+
+    @property
+    def total_bytes(self) -> int:
+        return self.sent_bytes + self.received_bytes
+
+    def count(self, sent: int, received: int) -> None:
+        self.sent_bytes += sent
+        self.received_bytes += received
+
+    def barrier(self, state=None) -> None:
+        self.fences += 1
+
+    def ensure_registered(self, state) -> None:
+        pass
+
+    def peer_pointer(self, state, rank: int) -> int:
+        if rank == self.rank:
+            raise TransportError(f"rank {rank} is this rank; no peer mapping")
+        return self.states[rank].amps.data_ptr()
+
+    def release(self, state) -> None:
+        pass
+
+    def close(self) -> None:
+        pass
+
+
 def execute_action(state: LocalState, action: GateAction, q: GateMatrix, fabric: NvlinkFabric | None,
                    executor=None) -> None:
     """Run one rank's share of one gate; fences bracket every exchange-class gate on all ranks."""
