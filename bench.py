@@ -39,7 +39,7 @@ METRIC = "gates/sec & effective HBM GB/s per gate vs 8 TB/s at n qubits; 1/2/4/8
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10, help="timed steps (BASELINE config 2: 10 repetitions of the sweep)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=["sweep", "controlled", "random", "qft"], default="sweep")
@@ -497,6 +497,8 @@ def main():
         # pinned host buffers for every rank on this node must fit comfortably in RAM
         local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
         pipelined = 2 * (16 << m) * local_world <= 0.45 * psutil.virtual_memory().total
+        free_dev = torch.cuda.mem_get_info(dev)[0]
+        nslot = 3 if free_dev > 3.5 * (16 << m) else 2  # three device slots: upload i+1 || download i-1
         h_in = torch.empty(lay.local_len, dtype=torch.complex128, pin_memory=True)
         h_out = torch.empty(lay.local_len, dtype=torch.complex128, pin_memory=True) if pipelined else h_in
         state.store_host(h_in)
@@ -506,7 +508,8 @@ def main():
         e0.record(stream)
         # every step: pinned H2D of its input, the circuit, D2H of its result
         if pipelined:  # public run_pipelined overlaps step i+1's upload / step i-1's download with step i
-            sv.run_pipelined(lay, timed, [h_in] * len(timed), [h_out] * len(timed), fabric, fusion=fcfg)
+            sv.run_pipelined(lay, timed, [h_in] * len(timed), [h_out] * len(timed), fabric, fusion=fcfg,
+                             slots=nslot)
         else:  # one host buffer per rank: sequential upload -> gates -> download
             for c in timed:
                 state.load_host(h_in)
@@ -521,7 +524,7 @@ def main():
                "h2d_bytes_per_step": (16 << m) * world, "d2h_bytes_per_step": (16 << m) * world,
                "ms_per_step": round(e2e_ms / len(timed), 3),
                "path": ("run_pipelined: LocalState.load_host (sv_copy, H2D stream) -> run_circuit -> "
-                        "LocalState.store_host (sv_copy, D2H stream), two device slots") if pipelined else
+                        f"LocalState.store_host (sv_copy, D2H stream), {nslot} device slots") if pipelined else
                        "sequential LocalState.load_host -> run_circuit -> store_host (host RAM bound)"}
         if rank == 0 and world == 1 and not args.no_cpu_baseline:
             cpu = cpu_baseline(sv, h_in, n, timed[0], args.cpu_seconds)

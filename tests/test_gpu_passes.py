@@ -158,13 +158,14 @@ def test_exchange_stage_abi_guards():
     assert L.sv_apply_gates(a.data_ptr(), 6, g, 1, 0, st) == _lib.SV_EINVAL  # target 6 not local
 
 
-def test_run_pipelined_matches_run_circuit():
+@pytest.mark.parametrize("slots", [2, 3])
+def test_run_pipelined_matches_run_circuit(slots):
     n = 16
     rng = np.random.default_rng(44)
-    circs = [sv.random_circuit(n, 30, rng, controlled_fraction=0.4) for _ in range(3)]
-    ins = [torch.from_numpy(random_state(rng, n)).pin_memory() for _ in range(3)]
+    circs = [sv.random_circuit(n, 30, rng, controlled_fraction=0.4) for _ in range(5)]
+    ins = [torch.from_numpy(random_state(rng, n)).pin_memory() for _ in range(5)]
     outs = [torch.empty_like(x).pin_memory() for x in ins]
-    sv.run_pipelined(sv.Layout(n), circs, ins, outs, fusion=sv.FusionConfig(l_c=12, passes=True))
+    sv.run_pipelined(sv.Layout(n), circs, ins, outs, fusion=sv.FusionConfig(l_c=12, passes=True), slots=slots)
     torch.cuda.synchronize()
     for c, x, y in zip(circs, ins, outs):
         want = run_oracle(x.numpy(), c.gates)
