@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--diagonal-local", action="store_true",
                     help="diagonal gates on global qubits without an exchange (SURVEY.md 8(f)1; off by default: "
                          "it departs from the reference's per-gate NVLink traffic contract)")
+    ap.add_argument("--remap", action="store_true",
+                    help="global<->local qubit swaps instead of per-gate exchanges (SURVEY.md 8(f)4; N > 1)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
@@ -290,16 +292,27 @@ def p2p_probe(state, fabric, dev, barrier, reduce_scalar, nbytes=1 << 31, reps=3
             "how": "cudaMemcpyAsync of the partner's (rank^1) CUDA-IPC-mapped slice, every rank at once"}
 
 
-def make_units(sv, circ, m, fusion, l_c, state, fabric):
-    """The launch groups of one step: (kind, algorithmic HBM bytes, gate count, callable).
+def make_units(sv, circ, m, fusion, l_c, state, fabric, remap=False):
+    """The launch groups of one step: (kind, bytes, gate count, callable, gates); bytes are
+    algorithmic HBM bytes for local units and NVLink bytes per direction for link units.
 
     Unfused: one unit per gate (the reference's engine.py:88-95 loop).  Passes:
-    one unit per HBM pass of the native planner (passes.py)."""
+    one unit per HBM pass of the native planner (passes.py).  remap: global<->local
+    swaps (remap.py) instead of exchanges, the gates in between as above."""
+    if remap and fabric is not None:
+        items, _ = sv.plan_remapped(circ.gates, circ.n, m)
+        units = []
+        for it in items:
+            if isinstance(it, sv.Swap):
+                units.append(("swap", 1 << (m + 3), 0, (lambda it=it: sv.swap_global(state, it, fabric)), ()))
+            else:
+                units += make_units(sv, sv.Circuit(circ.n, it), m, fusion, l_c, state, fabric)
+        return units
     if fusion == "passes":
         from paper_1601_07195_b200.passes import tile_for
 
         tile = tile_for(l_c, m)
-        return [("pass-" + p.kind, 32 << m, len(p.gates),
+        return [("pass-" + p.kind, (32 << m) if p.local else (1 << (m + 4)), len(p.gates),
                  (lambda p=p: sv.execute_pass(state, p, fabric, tile=tile)), p.gates)
                 for p in sv.plan_passes(circ.gates, m, tile)]
     units = []
@@ -378,7 +391,7 @@ def main():
 
     # ---------------------------------------------------------- warm-up
     for c in circs[: args.warmup]:
-        for _, _, _, fn, _ in make_units(sv, c, m, fusion, args.l_c, state, fabric):
+        for _, _, _, fn, _ in make_units(sv, c, m, fusion, args.l_c, state, fabric, args.remap):
             fn()
     barrier()
 
@@ -387,7 +400,7 @@ def main():
 
     # ------------------------------------------------ timed (device-resident)
     timed = circs[args.warmup:]
-    units = [make_units(sv, c, m, fusion, args.l_c, state, fabric) for c in timed]
+    units = [make_units(sv, c, m, fusion, args.l_c, state, fabric, args.remap) for c in timed]
     ev = []
     launches0 = sv.launch_count()
     with ClockSampler(local) as clocks:
@@ -463,11 +476,11 @@ def main():
         buckets = {k: {"gbps": round((16 << m) / (float(np.median(v)) * 1e-3) / 1e9, 1), "gates": len(v)}
                    for k, v in sorted(buckets.items())}
     nvlink = None
-    glob = [r for k, rs in by_kind.items() if k in ("exchange", "pass-global_stage", "pass-global_gate") for r in rs]
+    glob = [r for k, rs in by_kind.items() if k in ("exchange", "swap", "pass-global_stage", "pass-global_gate")
+            for r in rs]
     if world > 1 and glob:
-        per_dir = 1 << (m + 4)
         d = float(np.mean([r[1] for r in glob]))
-        ach = per_dir / (d * 1e-3) / 1e9
+        ach = sum(r[0] for r in glob) / (sum(r[1] for r in glob) * 1e-3) / 1e9  # link bytes per direction / time
         nvlink = {"achieved_gbs_per_direction": round(ach, 1),
                   "peak_nominal": 900.0, "peak_measured_p2p": p2p["gbs_per_direction"] if p2p else None,
                   "frac_nominal": round(ach / 900.0, 4),
@@ -542,6 +555,7 @@ def main():
                        "state_gib_per_gpu": (16 << m) / 2**30, "parallelism": f"state sharded over {world} GPU(s)",
                        "data_plane": fabric.data_plane if fabric is not None else None,
                        "diagonal_local": bool(fabric is not None and fabric.diag_mode),
+                       "remap": bool(args.remap and fabric is not None),
                        "l2": "no flush: slice >> 126 MB L2" if m >= 26 else "slice fits L2 (parity-size run)",
                        "seed": {"state": 0, "circuit": 1}},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "self_check": self_check,

@@ -156,6 +156,15 @@ int sv_diag_global(void *amps, int m, int own_is_zero, int c_local, const double
 int sv_diag_fix(void *amps, int m, int own_is_zero, int c_local, const double *q, const void *partner_signs,
                 const int *flag, void *stream);
 
+/* Swap global qubit G (the pairing bit of `theirs`) with local qubit l
+ * (communication-avoiding remapping): afterwards this rank
+ * holds the amplitudes whose bit G equals its bit l.  Elements with local bit
+ * l = 1 - b (b = this rank's bit G; own_is_zero = !b) trade places with the
+ * partner's elements with bit l = b: 2^(m+3) bytes per direction, half of an
+ * in-place exchange.  Both partners call it between two barriers; each moves
+ * half of the pairs.  2 <= m, 0 <= l < m. */
+int sv_swap_global(void *mine, void *theirs, int m, int own_is_zero, int l, void *stream);
+
 /* Sum of |a|^2 over the slice (qubit = -1) or over local bit `qubit` = 1
  * (core.py:147-167 partials).  Deterministic: fixed grid, fixed reduction
  * order.  `scratch` is a device buffer of SV_NORM_SCRATCH doubles; the result

@@ -65,6 +65,7 @@ from .distributed import (
 from .circuitfile import parse_circuit_file, parse_circuit_text
 from .engine import CircuitGraph, GateRecord, run_circuit, run_circuit_inproc, run_pipelined
 from .passes import Pass, execute_pass, plan_passes
+from .remap import QubitMap, Swap, plan_remapped, restore_map, run_circuit_remapped, swap_global
 from .errors import CircuitParseError, FusionContractError, LayoutError, ResourceError, TransportError
 from .fusion import (
     FusedBlockRun,

@@ -1167,6 +1167,41 @@ __global__ void __launch_bounds__(BLK) k_exchange(double2 *__restrict__ mine, do
   cta_release_system();
 }
 
+// ------------------------------------------------ global <-> local qubit swap
+//
+// SURVEY.md 8(f)4 (PAPER.md:478 future work): instead of exchanging for every
+// gate on a global qubit G, swap G with a local qubit l once -- afterwards the
+// logical qubit is local and its gates run in HBM.  With b the rank's bit G,
+// the swap moves (rank b, bit l = 1-b) <-> (rank 1-b, bit l = b): half of each
+// slice, 2^(m+3) B per direction (the in-place exchange moves 2^(m+4)).  One
+// thread owns each element pair (reads both, writes both), the zero side the
+// first half of the pair space, so the partners never race.  Pure data
+// movement: results stay bit-identical.
+__global__ void __launch_bounds__(BLK) k_swap_global(double2 *__restrict__ mine, double2 *__restrict__ theirs,
+                                                     uint64_t count, uint64_t j0, int l, int b) {
+  const uint64_t p0 = (uint64_t)blockIdx.x * (BLK * UNROLL) + threadIdx.x;
+  double2 x[UNROLL], y[UNROLL];
+  uint64_t im[UNROLL], it[UNROLL];
+#pragma unroll
+  for (int u = 0; u < UNROLL; ++u) {
+    const uint64_t p = p0 + (uint64_t)u * BLK;
+    const uint64_t j = j0 + p, z = insert_zero(j, l);
+    im[u] = b ? z : (z | (1ull << l));  // own half with bit l = 1 - b
+    it[u] = b ? (z | (1ull << l)) : z;  // partner half with bit l = b
+    if (p < count) {
+      x[u] = mine[im[u]];
+      y[u] = theirs[it[u]];
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < UNROLL; ++u) {
+    if (p0 + (uint64_t)u * BLK >= count) continue;
+    mine[im[u]] = y[u];
+    theirs[it[u]] = x[u];
+  }
+  cta_release_system();
+}
+
 // A whole stage of gates sharing one global target in ONE exchange: every
 // pair crosses NVLink once each way however many gates the stage holds
 // (controls: local bits -> per-element predicate; rank bits were resolved on
@@ -1840,6 +1875,17 @@ int sv_exchange_stage(void *mine, void *theirs, int m, int own_is_zero, const sv
     k_exchange_stage<0><<<grid, BLK, 0, (cudaStream_t)stream>>>((double2 *)mine, (double2 *)theirs, half,
                                                                 own_is_zero ? 0 : half, own_is_zero ? 1 : 0, P);
   return after_launch("sv_exchange_stage");
+}
+
+int sv_swap_global(void *mine, void *theirs, int m, int own_is_zero, int l, void *stream) {
+  if (bad_ptr(mine) || bad_ptr(theirs)) return fail(SV_EINVAL, "sv_swap_global: null or misaligned pointer");
+  if (mine == theirs) return fail(SV_EINVAL, "sv_swap_global: partner slice aliases the local slice");
+  if (m < 2 || m > 62) return fail(SV_EINVAL, "sv_swap_global: m=%d out of range", m);
+  if (l < 0 || l >= m) return fail(SV_EINVAL, "sv_swap_global: qubit %d not local (m=%d)", l, m);
+  const uint64_t quarter = 1ull << (m - 2);  // each side swaps half of the 2^(m-1) pairs
+  k_swap_global<<<grid_for(quarter, BLK * UNROLL), BLK, 0, (cudaStream_t)stream>>>(
+      (double2 *)mine, (double2 *)theirs, quarter, own_is_zero ? 0 : quarter, l, own_is_zero ? 0 : 1);
+  return after_launch("sv_swap_global");
 }
 
 int sv_exchange(void *mine, void *theirs, int m, int own_is_zero, int c_local, const double *q, void *stream) {

@@ -282,6 +282,11 @@ class CudaExecutor:
         with torch.cuda.device(state.amps.device):
             _lib.check(_lib.load().sv_copy(dst, src, nbytes, stream_handle()))
 
+    def swap_global(self, state: LocalState, theirs: int, own_is_zero: bool, l: int) -> None:
+        ptr, m = device_view(state.amps)
+        with torch.cuda.device(state.amps.device):
+            _lib.check(_lib.load().sv_swap_global(ptr, theirs, m, int(own_is_zero), int(l), stream_handle()))
+
     # --- diagonal global gates
     def diag_alloc(self, state: LocalState):
         """(sign map, flag) device buffers of sv_diag_global for this slice."""

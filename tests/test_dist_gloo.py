@@ -113,6 +113,17 @@ class ShmOracleExecutor:
             out += mat[1, 1] * x[sel]
         x[sel] = out
 
+    def swap_global(self, state, theirs, own_is_zero, l):
+        m = state.layout.m
+        w = np.frombuffer((ctypes.c_char * (16 << m)).from_address(theirs), dtype=np.complex128)
+        quarter = 1 << (m - 2)
+        j = np.arange(quarter, dtype=np.int64) + (0 if own_is_zero else quarter)
+        z = ((j >> l) << (l + 1)) | (j & ((1 << l) - 1))
+        im, it = (z | (1 << l), z) if own_is_zero else (z, z | (1 << l))
+        x = state.amps[im].copy()
+        state.amps[im] = w[it]
+        w[it] = x
+
     def cleanup(self):
         for shm in getattr(self, "_own", []):
             shm.close()
@@ -393,3 +404,73 @@ def test_gloo_diagonal_local_protocol(world, n):
     # in every uncontrolled one; none for the diagonal ones
     assert int(out["sent"]) <= sum(1 << (m + 4) for _ in exch)
     assert int(out["fences"]) == 2 * sum(1 for o in glob if o.target >= m) + 1
+
+
+def _worker_remap(rank, world, port, path, n):
+    """run_circuit_remapped: global<->local swaps instead of per-gate exchanges."""
+    import torch.distributed as dist
+
+    import paper_1601_07195_b200 as sv
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        p = world.bit_length() - 1
+        d = dict(np.load(path + ".npz"))
+        lay = sv.Layout(n, p, rank)
+        m = lay.m
+        shm = shared_memory.SharedMemory(create=True, size=16 << m, name=f"svr_{os.getpid()}_{rank}")
+        amps = np.ndarray((1 << m,), dtype=np.complex128, buffer=shm.buf)
+        amps[:] = d["init"][rank << m:(rank + 1) << m]
+        state = ShmState(lay, amps, shm)
+        ex = ShmOracleExecutor()
+        fabric = sv.NvlinkFabric(fence="host", executor=ex)
+        circ = sv.Circuit(n, [sv.GateOp(sv.GateMatrix.unchecked(q.reshape(2, 2)), int(t), None if c < 0 else int(c))
+                              for t, c, q in zip(d["t"], d["c"], d["q"])])
+        qm = sv.run_circuit_remapped(state, circ, fabric, executor=ex)
+        fabric.barrier()
+        pids = fabric.exchange_objects(os.getpid())
+        if rank == 0:
+            parts = [amps.copy()]
+            for r in range(1, world):
+                other = shared_memory.SharedMemory(name=f"svr_{pids[r]}_{r}")
+                parts.append(np.ndarray((1 << m,), dtype=np.complex128, buffer=other.buf).copy())
+                other.close()
+            np.savez(path + ".out.npz", full=np.concatenate(parts), sent=fabric.sent_bytes, ident=qm.identity)
+        fabric.barrier()
+        fabric.close()
+        del amps
+        shm.close()
+        shm.unlink()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n", [(2, 8), (4, 9), (8, 10)])
+def test_gloo_remapped_execution(world, n):
+    """QFT + random gates with global<->local swaps over real ranks: the
+    oracle's state, the identity map at the end, and fewer link bytes than the exchanges."""
+    import torch.multiprocessing as mp
+
+    import paper_1601_07195_b200 as sv
+    from conftest import random_state
+    from oracle import oracle
+
+    p = world.bit_length() - 1
+    m = n - p
+    rng = np.random.default_rng(world * 11 + n)
+    circ = sv.build_qft(n)
+    circ.extend(sv.random_circuit(n, 60, rng, controlled_fraction=0.4).gates)
+    init = random_state(rng, n)
+    want = init.copy()
+    oracle.run_circuit(want, circ.gates)
+    with tempfile.TemporaryDirectory() as tmp:
+        path = os.path.join(tmp, "r")
+        np.savez(path + ".npz", init=init, t=np.array([o.target for o in circ]),
+                 c=np.array([-1 if o.control is None else o.control for o in circ]),
+                 q=np.stack([o.gate.mat.reshape(4) for o in circ]))
+        mp.spawn(_worker_remap, args=(world, _port(), path, n), nprocs=world, join=True)
+        out = dict(np.load(path + ".out.npz"))
+    assert np.array_equal(out["full"], want) and bool(out["ident"])
+    items, _ = sv.plan_remapped(circ.gates, n, m)
+    assert int(out["sent"]) == sum(isinstance(i, sv.Swap) for i in items) << (m + 3)
+    assert int(out["sent"]) < sum(1 for o in circ if o.target >= m) << (m + 4)
