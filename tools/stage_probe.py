@@ -69,6 +69,10 @@ cases = {
     "phase_hi_unctl_60": [sv.GateOp(sv.phase_r(3), n - 1)] * 60,
     "phase_hi_unctl_110": [sv.GateOp(sv.phase_r(3), n - 1)] * 110,
     "phase_4slots_ctl_hi_110": [sv.GateOp(sv.phase_r(3), n - 1 - (i % 4), 10 + (i % 15)) for i in range(110)],
+    "phase_ctl_one_hi_110": [sv.GateOp(sv.phase_r(3), n - 1, 15)] * 110,
+    "phase_ctl_two_hi_110": [sv.GateOp(sv.phase_r(3), n - 1, 15 + (i % 2)) for i in range(110)],
+    "phase_ctl_8bits_hi_110": [sv.GateOp(sv.phase_r(3), n - 1, 10 + (i % 8)) for i in range(110)],
+    "phase_ctl_blocks_hi_110": [sv.GateOp(sv.phase_r(3), n - 1, 10 + i // 10) for i in range(110)],
     "general_hi_30": [sv.GateOp(sv.random_unitary(np.random.default_rng(i)), n - 1 - (i % 4)) for i in range(30)],
 }
 res = {"n": n}
