@@ -492,7 +492,9 @@ def main():
     if initial is not None:
         for c in reversed(circs):
             sv.run_circuit(state, c.inverse(), fabric, fusion=fcfg)
-        err = float((state.amps - initial).abs().max().item())
+        from paper_1601_07195_b200.core import max_abs_diff
+
+        err = max_abs_diff(state.amps, initial)
         if world > 1:
             err = reduce_scalar(err, dist.ReduceOp.MAX)
         ng = 2 * sum(len(c) for c in circs)

@@ -171,6 +171,11 @@ int sv_swap_global(void *mine, void *theirs, int m, int own_is_zero, int l, void
  * lands in scratch[SV_NORM_SCRATCH - 1]. */
 int sv_norm_sq(const void *amps, int m, int qubit, double *scratch, void *stream);
 
+/* max_i |a_i - b_i| (complex modulus) over two slices of 2^m amplitudes (the bench's
+ * full-size self-check: a circuit followed by its inverse restores the input).
+ * Result in scratch[SV_NORM_SCRATCH - 1], as sv_norm_sq. */
+int sv_max_abs_diff(const void *a, const void *b, int m, double *scratch, void *stream);
+
 /* Seeded i.i.d. complex Gaussian amplitudes (Philox4x32-10 + Box-Muller),
  * element j of rank r drawn from counter (r << m) + j, so a sharded state
  * equals the unsharded one.  Not normalised: follow with sv_norm_sq/sv_scale. */

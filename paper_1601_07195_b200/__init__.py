@@ -30,6 +30,7 @@ from .circuits import (
     rotation_z,
 )
 from .core import (
+    max_abs_diff,
     ALIGNMENT,
     AMP_BYTES,
     Layout,

@@ -29,7 +29,7 @@ EXPORTS = (
     "sv_apply_fused", "sv_apply_gates", "sv_plan_gates", "sv_apply_group", "sv_exchange", "sv_exchange_chunk",
     "sv_exchange_stage", "sv_norm_sq", "sv_init_random", "sv_scale", "sv_init_basis",
     "sv_copy", "sv_ipc_handle", "sv_ipc_open", "sv_ipc_close", "sv_diag_global", "sv_diag_fix",
-    "sv_swap_global",
+    "sv_swap_global", "sv_max_abs_diff",
 )
 
 
@@ -84,6 +84,7 @@ def load() -> ctypes.CDLL:
         "sv_diag_global": ([vp, i, i, i, dp, vp, vp, vp], i),
         "sv_diag_fix": ([vp, i, i, i, dp, vp, vp, vp], i),
         "sv_swap_global": ([vp, vp, i, i, i, vp], i),
+        "sv_max_abs_diff": ([vp, vp, i, vp, vp], i),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

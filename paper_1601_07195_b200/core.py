@@ -177,6 +177,18 @@ def _reduce_sum(partial: float, layout: Layout, transport: "NvlinkFabric | None"
     return transport.reduce_sum(partial)
 
 
+def max_abs_diff(a: torch.Tensor, b: torch.Tensor) -> float:
+    """max |a_i - b_i| over two device slices of the same length (sv_max_abs_diff)."""
+    pa, m = device_view(a)
+    pb, mb = device_view(b)
+    if m != mb:
+        raise ValueError(f"slices differ in length: 2^{m} vs 2^{mb}")
+    scratch = torch.empty(_lib.SV_NORM_SCRATCH, dtype=torch.float64, device=a.device)
+    with torch.cuda.device(a.device):
+        _lib.check(_lib.load().sv_max_abs_diff(pa, pb, m, scratch.data_ptr(), stream_handle()))
+    return float(scratch[-1].item())
+
+
 def global_norm_sq(state: LocalState, transport: "NvlinkFabric | None" = None) -> float:
     """Sum of |amplitude|^2 over the whole state (core.py:147-150)."""
     return _reduce_sum(_partial_norm(state, -1), state.layout, transport)

@@ -1283,6 +1283,40 @@ __global__ void __launch_bounds__(BLK) k_norm_final(double *__restrict__ partial
   if (threadIdx.x == 0) partial[NORM_BLOCKS] = red[0];
 }
 
+// max |a_i - b_i| (complex modulus) over two slices: the full-size self-checks (a circuit
+// then its inverse restores the input).  Fixed grid; max is order-independent.
+__global__ void __launch_bounds__(BLK) k_maxdiff_partial(const double2 *__restrict__ a,
+                                                         const double2 *__restrict__ b, uint64_t n,
+                                                         double *__restrict__ partial) {
+  __shared__ double red[BLK];
+  double acc = 0.0;
+  const uint64_t stride = (uint64_t)NORM_BLOCKS * BLK;
+  for (uint64_t i = (uint64_t)blockIdx.x * BLK + threadIdx.x; i < n; i += stride) {
+    const double2 x = a[i], y = b[i];
+    acc = fmax(acc, hypot(x.x - y.x, x.y - y.y));  // NaN-free inputs: fmax keeps the max
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = BLK / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
+}
+
+__global__ void __launch_bounds__(BLK) k_max_final(double *__restrict__ partial) {
+  __shared__ double red[BLK];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < NORM_BLOCKS; i += BLK) acc = fmax(acc, partial[i]);
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = BLK / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[NORM_BLOCKS] = red[0];
+}
+
 // Philox4x32-10 (Salmon et al., SC'11), counter = global amplitude index.
 __device__ __forceinline__ uint4 philox(uint4 ctr, uint2 key) {
   const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u, W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;
@@ -1971,6 +2005,15 @@ int sv_norm_sq(const void *amps, int m, int qubit, double *scratch, void *stream
   k_norm_partial<<<NORM_BLOCKS, BLK, 0, st>>>((const double2 *)amps, 1ull << m, qubit, scratch);
   k_norm_final<<<1, BLK, 0, st>>>(scratch);
   return after_launch("sv_norm_sq", 2);
+}
+
+int sv_max_abs_diff(const void *a, const void *b, int m, double *scratch, void *stream) {
+  if (bad_ptr(a) || bad_ptr(b) || !scratch) return fail(SV_EINVAL, "sv_max_abs_diff: null or misaligned pointer");
+  if (m < 0 || m > 62) return fail(SV_EINVAL, "sv_max_abs_diff: m=%d out of range", m);
+  cudaStream_t st = (cudaStream_t)stream;
+  k_maxdiff_partial<<<NORM_BLOCKS, BLK, 0, st>>>((const double2 *)a, (const double2 *)b, 1ull << m, scratch);
+  k_max_final<<<1, BLK, 0, st>>>(scratch);
+  return after_launch("sv_max_abs_diff", 2);
 }
 
 int sv_init_random(void *amps, int m, uint64_t seed, uint64_t rank, void *stream) {

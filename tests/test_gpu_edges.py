@@ -102,3 +102,15 @@ def test_basis_states_and_probabilities_sharded():
         assert abs(sv.probability_of_bit(st, b) - want) < 1e-14
     with pytest.raises(ValueError):
         sv.probability_of_bit(st, 6)
+
+
+def test_max_abs_diff_kernel():
+    """sv_max_abs_diff (the bench self-check) against numpy, including a single far element."""
+    rng = np.random.default_rng(5)
+    for n in (0, 3, 10, 17):
+        a = random_state(rng, n) if n else np.array([0.3 + 0.4j])
+        b = a + (rng.standard_normal(a.shape) + 1j * rng.standard_normal(a.shape)) * 1e-9
+        b[-1] += 0.25j
+        want = float(np.max(np.abs(a - b)))
+        got = sv.max_abs_diff(torch.from_numpy(a).to(DEV), torch.from_numpy(b).to(DEV))
+        assert got == pytest.approx(want, rel=1e-15, abs=0)
