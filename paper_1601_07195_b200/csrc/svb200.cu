@@ -1076,23 +1076,36 @@ __global__ void __launch_bounds__(MS_BLK, SV_MS_MINB * 256 / MS_BLK) k_mstage(do
 
 __global__ void __launch_bounds__(BLK) k_diag_global(double2 *__restrict__ a, uint64_t n, int c, double dr,
                                                      double di, uint32_t *__restrict__ signs, int *flag) {
-  const uint64_t stride = (uint64_t)gridDim.x * BLK;
-  const uint64_t npad = (n + 31) & ~31ull;
+  // each warp takes DG consecutive 32-element groups per iteration, loads first (ILP)
+  constexpr int DG = 4;
+  const int lane = threadIdx.x & 31;
+  const uint64_t warp = ((uint64_t)blockIdx.x * BLK + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * BLK) >> 5;
+  const uint64_t ngroups = (n + 31) >> 5;
   bool zero = false;
-  for (uint64_t i = (uint64_t)blockIdx.x * BLK + threadIdx.x; i < npad; i += stride) {
-    const bool act = i < n && (c < 0 || ((i >> c) & 1ull));
-    double2 x = make_double2(0.0, 0.0);
-    if (act) x = a[i];
-    const uint32_t sre = __ballot_sync(0xffffffffu, act && signbit(x.x));
-    const uint32_t sim = __ballot_sync(0xffffffffu, act && signbit(x.y));
-    if ((threadIdx.x & 31) == 0 && (c < 5 || ((i >> c) & 1ull))) {
-      signs[2 * (i >> 5)] = sre;
-      signs[2 * (i >> 5) + 1] = sim;
+  for (uint64_t g0 = warp * DG; g0 < ngroups; g0 += nwarps * DG) {
+    double2 x[DG];
+    bool act[DG];
+#pragma unroll
+    for (int u = 0; u < DG; ++u) {
+      const uint64_t i = ((g0 + u) << 5) + lane;
+      act[u] = g0 + u < ngroups && i < n && (c < 0 || ((i >> c) & 1ull));
+      x[u] = act[u] ? a[i] : make_double2(0.0, 0.0);
     }
-    if (act) {
-      const double2 pv = cmul(dr, di, x);
-      zero |= !nonzero2(pv);
-      a[i] = pv;
+#pragma unroll
+    for (int u = 0; u < DG; ++u) {
+      const uint64_t g = g0 + u;
+      const uint32_t sre = __ballot_sync(0xffffffffu, act[u] && signbit(x[u].x));
+      const uint32_t sim = __ballot_sync(0xffffffffu, act[u] && signbit(x[u].y));
+      if (lane == 0 && g < ngroups && (c < 5 || (((g << 5) >> c) & 1ull))) {
+        signs[2 * g] = sre;
+        signs[2 * g + 1] = sim;
+      }
+      if (act[u]) {
+        const double2 pv = cmul(dr, di, x[u]);
+        zero |= !nonzero2(pv);
+        a[(g << 5) + lane] = pv;
+      }
     }
   }
   if (__syncthreads_or(zero) && threadIdx.x == 0) atomicOr(flag, 1);
