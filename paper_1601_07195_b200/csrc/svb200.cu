@@ -1001,6 +1001,48 @@ __device__ __forceinline__ void ms_exact(double2 (&r)[MS_N], int cs, const doubl
   }
 }
 
+// All-zero groups (basis states and the sparse early stages of their transforms) through a
+// whole pass on SIGN BITS: zeros stay zeros under mix(), and the IEEE sign of each result
+// is a boolean function of the operands' signs -- a product of zeros has the XOR of the
+// signs, a round-to-nearest sum (or fma addend) of two zeros is -0 only if both are.  With
+// the 16 real and 16 imaginary signs of the group packed in two words, cmul(r, x) of every
+// pair at once is re = (r.re ^ x.re) & ~(x.im ^ r.im), im = (r.re ^ x.im) & (x.re ^ r.im)
+// (cmul's fma(rr, x.re, -(x.im * ri)) and fma(rr, x.im, x.re * ri)), and mix() ANDs two of
+// them: ~25 integer ops per gate instead of 160 FP64 ops, bit-identical to mix().
+__device__ __forceinline__ uint32_t sgn_mask(double v) { return signbit(v) ? 0xFFFFu : 0u; }
+
+__device__ __noinline__ void ms_replay_zero(double2 *__restrict__ a, uint64_t base, const MsParams *P,
+                                            const uint64_t (&b)[MS_K], uint32_t sre, uint32_t sim) {
+  for (int gi = 0; gi < P->ngates; ++gi) {
+    const int c = P->cbit[gi];
+    if (c != 0xFF && !((base >> c) & 1ull)) continue;
+    const int code = P->g[gi].code;
+    const int cs = code % (MS_K + 1), s = (code / (MS_K + 1)) % MS_K;
+    const double *q = P->g[gi].q;
+    // pairs (j, j | 1<<s) with bit s of j clear (and bit cs set for a slot control)
+    uint32_t m0 = 0;
+#pragma unroll
+    for (int j = 0; j < MS_N; ++j)
+      if (!((j >> s) & 1) && (cs >= MS_K || ((j >> cs) & 1))) m0 |= 1u << j;
+    const int sh = 1 << s;
+    const uint32_t a0r = sre & m0, a0i = sim & m0, a1r = (sre >> sh) & m0, a1i = (sim >> sh) & m0;
+    auto cm_re = [&](int k, uint32_t xr, uint32_t xi) {
+      return (sgn_mask(q[2 * k]) ^ xr) & ~(xi ^ sgn_mask(q[2 * k + 1])) & m0;
+    };
+    auto cm_im = [&](int k, uint32_t xr, uint32_t xi) {
+      return (sgn_mask(q[2 * k]) ^ xi) & (xr ^ sgn_mask(q[2 * k + 1])) & m0;
+    };
+    const uint32_t n0r = cm_re(0, a0r, a0i) & cm_re(1, a1r, a1i), n0i = cm_im(0, a0r, a0i) & cm_im(1, a1r, a1i);
+    const uint32_t n1r = cm_re(2, a0r, a0i) & cm_re(3, a1r, a1i), n1i = cm_im(2, a0r, a0i) & cm_im(3, a1r, a1i);
+    const uint32_t keep = ~(m0 | (m0 << sh));
+    sre = (sre & keep) | n0r | (n1r << sh);
+    sim = (sim & keep) | n0i | (n1i << sh);
+  }
+#pragma unroll
+  for (int j = 0; j < MS_N; ++j)
+    a[base | ms_off(j, b)] = make_double2((sre >> j) & 1u ? -0.0 : 0.0, (sim >> j) & 1u ? -0.0 : 0.0);
+}
+
 // Exact replay of one thread's group from global memory (nothing stored yet).
 __device__ __noinline__ void ms_replay(double2 *__restrict__ a, uint64_t base, const MsParams *P) {
   uint64_t b[MS_K];
@@ -1009,6 +1051,19 @@ __device__ __noinline__ void ms_replay(double2 *__restrict__ a, uint64_t base, c
   double2 r[MS_N];
 #pragma unroll
   for (int j = 0; j < MS_N; ++j) r[j] = a[base | ms_off(j, b)];
+  bool allzero = true;
+  uint32_t sre = 0, sim = 0;
+#pragma unroll
+  for (int j = 0; j < MS_N; ++j) {
+    allzero &= ((__double2hiint(r[j].x) & 0x7fffffff) | __double2loint(r[j].x) |
+                (__double2hiint(r[j].y) & 0x7fffffff) | __double2loint(r[j].y)) == 0;
+    sre |= (signbit(r[j].x) ? 1u : 0u) << j;
+    sim |= (signbit(r[j].y) ? 1u : 0u) << j;
+  }
+  if (allzero) {
+    ms_replay_zero(a, base, P, b, sre, sim);
+    return;
+  }
   for (int gi = 0; gi < P->ngates; ++gi) {
     const int c = P->cbit[gi];
     if (c != 0xFF && !((base >> c) & 1ull)) continue;

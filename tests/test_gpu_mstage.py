@@ -127,3 +127,29 @@ def test_stage_tiny_slices_partial_warps(n):
         apply_stage(a, ops)
         torch.cuda.synchronize()
         assert bits_equal(a.cpu().numpy(), run_oracle(v, ops)), (n, trial)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_stage_all_zero_groups_sign_replay(seed):
+    """Groups whose 16 amplitudes are all +-0 replay on sign bits (ms_replay_zero): random zero
+    signs in whole zero blocks, every gate kind, slot / warp / CTA / lane controls."""
+    n = 16
+    rng = np.random.default_rng(900 + seed)
+    v = random_state(rng, n)
+    idx = np.arange(1 << n)
+    dead = ((idx >> 11) & 3) != 0  # three quarters of the state in whole zero blocks
+    f = v.view(np.float64).reshape(-1, 2)
+    f[dead] = np.where(rng.random((dead.sum(), 2)) < 0.5, 0.0, -0.0)
+    for targets in ([7, 8, 9, 10], [0, 3, 5, 9], [2, 6]):
+        ops = stage_ops(rng, n, targets, 100, cfrac=0.7)
+        a = torch.from_numpy(v.copy()).to(DEV)
+        apply_stage(a, ops)
+        torch.cuda.synchronize()
+        assert bits_equal(a.cpu().numpy(), run_oracle(v, ops)), targets
+    basis = np.zeros(1 << n, dtype=np.complex128)
+    basis[int(rng.integers(1 << n))] = 1.0
+    ops = stage_ops(rng, n, [12, 13, 14, 15], 120)
+    a = torch.from_numpy(basis.copy()).to(DEV)
+    apply_stage(a, ops)
+    torch.cuda.synchronize()
+    assert bits_equal(a.cpu().numpy(), run_oracle(basis, ops))
