@@ -875,6 +875,7 @@ struct MsGate {
 // at chunk bits lo..hi.  The kernel dispatches once per run and loops over the
 // run's gates that act in the warp with the update compiled for that code.
 struct MsRun {
+  uint32_t range;  // chunk bits lo..hi of the run, precomputed on the host
   uint8_t code, h, lo, hi;
 };
 
@@ -983,7 +984,7 @@ __device__ __forceinline__ void ms_run(double2 (&r)[MS_N], uint64_t base, const 
   }
   for (int ri = 0; ri < P.nruns; ++ri) {
     const MsRun R = P.run[ri];
-    const uint32_t range = (R.hi == 31 ? 0xffffffffu : ((2u << R.hi) - 1u)) & ~((1u << R.lo) - 1u);
+    const uint32_t range = R.range;
     const uint32_t mh = R.h == 0 ? M0 : R.h == 1 ? M1 : R.h == 2 ? M2 : M3;
     const uint32_t lh = R.h == 0 ? L0 : R.h == 1 ? L1 : R.h == 2 ? L2 : L3;
     const uint32_t act = mh & range;
@@ -1705,6 +1706,10 @@ int run_mstage(double2 *a, int m, const sv_gate *gates, int n, cudaStream_t st) 
     P.run[P.nruns].hi = (uint8_t)(k % 32);
   }
   ++P.nruns;
+  for (int ri = 0; ri < P.nruns; ++ri) {
+    MsRun &R = P.run[ri];
+    R.range = (R.hi == 31 ? 0xffffffffu : ((2u << R.hi) - 1u)) & ~((1u << R.lo) - 1u);
+  }
   const uint64_t ng = 1ull << (m - MS_K);
   k_mstage<<<grid_for(ng, MS_BLK), MS_BLK, 0, st>>>(a, ng, P);
   return after_launch("k_mstage");
