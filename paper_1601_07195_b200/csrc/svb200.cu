@@ -18,6 +18,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdarg>
+#include <cstddef>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
@@ -883,8 +884,8 @@ struct MsParams {
   int32_t ngates;
   int32_t nruns;
   int32_t bits[MS_K];     // slice bit of each slot, ascending
-  int32_t pad;
-  uint8_t cbit[MS_MAX];   // control of gate g when it is not a slot bit, else 0xFF
+  alignas(8) uint8_t cbit[MS_MAX];  // control of gate g when it is not a slot bit, else 0xFF
+                                    // (read 8 at a time: the alignment is required)
   MsRun run[MS_MAX + MS_MAX / 32];
   MsGate g[MS_MAX];
 };
@@ -962,6 +963,7 @@ __device__ __forceinline__ void ms_run(double2 (&r)[MS_N], uint64_t base, const 
   vary = ((uint64_t)__reduce_or_sync(0xffffffffu, (unsigned)(vary >> 32)) << 32) |
          __reduce_or_sync(0xffffffffu, (unsigned)vary);
   const uint64_t *cw = reinterpret_cast<const uint64_t *>(P.cbit);  // 8 control bytes per word
+  static_assert(offsetof(MsParams, cbit) % 8 == 0, "cbit words must be 8-byte aligned");
   static_assert(MS_MAX == 128, "four ballot chunks");
   uint32_t M0 = 0, M1 = 0, M2 = 0, M3 = 0, L0 = 0, L1 = 0, L2 = 0, L3 = 0;
 #pragma unroll
