@@ -61,8 +61,9 @@ class Swap:
 
 
 def plan_remapped(gates, n: int, m: int, restore: bool = True, qmap: QubitMap | None = None):
-    """Items in execution order: lists of PHYSICAL GateOps (every target local) and Swap
-    records.  Returns (items, final map)."""
+    """Items in execution order: lists of PHYSICAL GateOps and Swap records.  Every target
+    is local except when all local qubits are already displaced (more global than local
+    qubits); such a gate runs as the reference's in-place exchange.  Returns (items, map)."""
     gates = list(gates)
     qm = qmap or QubitMap(n)
     uses: dict[int, list[int]] = {}
@@ -89,8 +90,10 @@ def plan_remapped(gates, n: int, m: int, restore: bool = True, qmap: QubitMap | 
             else:
                 busy = {qm.pos[q] for q in op.qubits()}
                 cands = [b for b in range(m) if qm.occ[b] == b and b not in busy]
-                if not cands:
-                    raise LayoutError(f"no local qubit free to swap with global qubit {t} (m={m})")
+                if not cands:  # every local qubit is displaced (more global than local qubits):
+                    c = None if op.control is None else qm.pos[op.control]  # exchange in place
+                    cur.append(GateOp(op.gate, t, c, op.name))
+                    continue
                 victim = max(cands, key=lambda b: (next_use(b, i + 1), b))
             if cur:
                 items.append(cur)

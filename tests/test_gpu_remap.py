@@ -48,7 +48,7 @@ def test_swap_global_is_a_bit_permutation(n, p):
 
 
 @pytest.mark.parametrize("n,p,fusion", [(10, 1, None), (12, 2, None), (12, 2, "passes"), (14, 3, "passes"),
-                                        (14, 3, 5)])
+                                        (14, 3, 5), (8, 5, None)])
 def test_remapped_circuits_match_oracle_bitwise(n, p, fusion):
     m = n - p
     rng = np.random.default_rng(100 + n + p)

@@ -81,3 +81,18 @@ def test_link_traffic_of_the_baseline_circuits():
     circ = sv.random_circuit(36, 100, np.random.default_rng(1), controlled_fraction=0.0)
     items, _ = sv.plan_remapped(circ.gates, 36, 33)
     assert sum(isinstance(it, sv.Swap) for it in items) <= sum(op.target >= 33 for op in circ)
+
+
+def test_more_global_than_local_qubits_falls_back_to_exchanges():
+    n, m = 6, 2  # four global qubits, two local
+    rng = np.random.default_rng(12)
+    circ = sv.random_circuit(n, 80, rng, controlled_fraction=0.3)
+    v = random_state(rng, n)
+    want = v.copy()
+    oracle.run_circuit(want, circ.gates)
+    items, qm = sv.plan_remapped(circ.gates, n, m)
+    assert qm.identity
+    # the emulation applies physical gates with the oracle, exchanges included
+    got = emulate(v, items)
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+    assert any(op.target >= m for it in items if not isinstance(it, sv.Swap) for op in it)
