@@ -58,6 +58,10 @@ def main():
         "tile_qft12_ms": timed(lambda: sv.kernels.apply_gates(st.amps, diag, tile=12), reps),
         "qft_ms": timed(lambda: sv.run_circuit(st, qft, fusion=fc), reps),
     }
+    for lc in (12, 11):
+        steps = [[sv.GateOp(sv.random_unitary(rng), int(rng.integers(n))) for _ in range(25)] for _ in range(4)]
+        fl = sv.FusionConfig(l_c=lc, passes=True)
+        res[f"random25_lc{lc}_ms"] = timed(lambda: [sv.run_circuit(st, sv.Circuit(n, g), fusion=fl) for g in steps], reps) / 4
     b = sv.init_basis_state(sv.Layout(n), 5)
     res["qft_basis_ms"] = timed(lambda: sv.run_circuit(b, qft, fusion=fc), 1)
     print(json.dumps(res))
