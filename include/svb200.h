@@ -92,7 +92,9 @@ int sv_apply_gates(void *amps, int m, const sv_gate *gates, int ngates, int tile
 
 /* Launch-group kinds of the pass planner. */
 #define SV_GROUP_GATES 0 /* one launch per gate (sv_apply_single / sv_apply_controlled) */
-#define SV_GROUP_TILE 1  /* register-tiled run: targets < tile-4 plus up to four higher bits */
+#define SV_GROUP_TILE 1  /* register-tiled run: targets < tile-SV_TILE_GATHER plus up to SV_TILE_GATHER higher bits */
+/* Slice bits a register tile gathers (its top tile bits; the rest are runs of 2^(tile-8) amplitudes). */
+#define SV_TILE_GATHER 8
 #define SV_GROUP_STAGE 2 /* stage: targets in <= SV_MSTAGE_MAX_TARGETS qubits, 16 amplitudes per thread */
 
 /* The planner of sv_apply_gates, exposed (pure host code, no GPU needed):

@@ -339,6 +339,13 @@ static_assert(TR == 3 || TR == 4, "tile register bits");
 #define SV_TILE_MINB 2  // CTAs per SM for T <= 12 tiles (measured: 1 CTA with 255 registers is 1.6x slower)
 #endif
 constexpr int TRN = 1 << TR;
+#ifndef SV_TILE_G
+#define SV_TILE_G SV_TILE_GATHER  // gathered slice bits per tile (the top G tile bits; runs of 2^(T-G) amplitudes).
+// Measured (random config-4-shape steps of 25 Haar gates, n = 30, T = 12): G = 4/5/6/7/8/9 ->
+// 32.7/31.9/31.4/28.8/27.2/27.4 ms (fewer passes per circuit; same per-pass time).
+#endif
+constexpr int TG_BITS = SV_TILE_G;
+static_assert(TG_BITS >= TR && TG_BITS <= 9, "gathered tile bits: TR..9 (T >= 9)");
 constexpr uint32_t TFULL = (1u << TRN) - 1u;  // every register pair of a gate active
 
 // registers j whose register bit b is set (a control on register bit b)
@@ -347,7 +354,7 @@ __host__ __device__ constexpr uint32_t reg_mask(int b) {
 }
 
 struct TileHB {
-  int v[TR];
+  int v[TG_BITS];
 };
 constexpr int TILE_MAX_GATES = 256;
 constexpr int TILE_MAX_SEGS = 64;
@@ -370,24 +377,26 @@ struct TileSeg {
   int8_t pad[2];
 };
 
-// A tile is 2^T amplitudes: tile bits 0..T-5 are slice bits 0..T-5 (contiguous
-// runs, coalesced), tile bits T-4..T-1 are the slice bits hb[0..3] (ascending,
-// any positions >= T-4).  hb = {T-4, .., T-1} is the contiguous block of the
-// reference's apply_block; other choices put high qubits into the tile so runs
-// of gates on arbitrary targets fuse (the tile then is a strided gather).
+// A tile is 2^T amplitudes: tile bits 0..T-G-1 are slice bits 0..T-G-1
+// (contiguous runs, coalesced), tile bits T-G..T-1 are the slice bits
+// hb[0..G-1] (G = TG_BITS, ascending, any positions >= T-G).  hb = {T-G, ..,
+// T-1} is the contiguous block of the reference's apply_block; other choices
+// put high qubits into the tile so runs of gates on arbitrary targets fuse
+// (the tile then is a strided gather).  The natural register layout: thread
+// bits = tile bits 0..T-TR-1, register bits = tile bits T-TR..T-1.
 struct TileParams {
   int nsegs;
   int last_natural;
-  int hb[TR];
+  int hb[TG_BITS];
   TileSeg seg[TILE_MAX_SEGS];
   TileGate g[TILE_MAX_GATES];
 };
 
 template <int T>
-__device__ __forceinline__ uint64_t tile_base(uint64_t b, const int (&hb)[TR]) {
-  uint64_t x = b << (T - TR);
+__device__ __forceinline__ uint64_t tile_base(uint64_t b, const int (&hb)[TG_BITS]) {
+  uint64_t x = b << (T - TG_BITS);
 #pragma unroll
-  for (int k = 0; k < TR; ++k) x = insert_zero(x, hb[k]);
+  for (int k = 0; k < TG_BITS; ++k) x = insert_zero(x, hb[k]);
   return x;
 }
 
@@ -404,14 +413,17 @@ __device__ __forceinline__ int swz(int i) {
 // turns the 16 addresses into one XOR each (instead of ~9 ALU ops per address).
 // Global load / store of a thread's natural-layout registers: the offsets
 // tid | XOR_{k in j} 2^hb[k] (disjoint bits), visited in Gray-code order.
-template <bool STORE>
+template <int T, bool STORE>
 __device__ __forceinline__ void tile_gxfer(double2 *__restrict__ a, double2 (&r)[TRN], uint64_t tile0, int tid,
-                                           const int (&hb)[TR]) {
-  uint64_t off = tile0 | (uint64_t)tid;  // tile0 is zero on every tile bit
+                                           const int (&hb)[TG_BITS]) {
+  constexpr int L = T - TG_BITS, RB = TG_BITS - TR;  // contiguous bits; gathered bits held by threads
+  uint64_t off = tile0 | (uint64_t)(tid & ((1 << L) - 1));  // tile0 is zero on every tile bit
+#pragma unroll
+  for (int k = 0; k < RB; ++k) off |= (uint64_t)((tid >> (L + k)) & 1) << hb[k];
 #pragma unroll
   for (int i = 0; i < TRN; ++i) {
     const int g = i ^ (i >> 1);
-    if (i) off ^= 1ull << hb[(i & 1) ? 0 : (i & 2) ? 1 : (i & 4) ? 2 : 3];
+    if (i) off ^= 1ull << hb[RB + ((i & 1) ? 0 : (i & 2) ? 1 : (i & 4) ? 2 : 3)];
     if (STORE)
       a[off] = r[g];
     else
@@ -510,10 +522,10 @@ __device__ __forceinline__ void tile_gate_k(double2 (&r)[TRN], uint32_t pm, cons
 // One tile through the run: load (natural layout), segments with transposes,
 // back to the natural layout in registers (the caller stores).
 template <int T, bool SPEC>
-__device__ __forceinline__ void tile_body(const double2 *__restrict__ a, uint64_t tile0, const int (&hb)[TR],
+__device__ __forceinline__ void tile_body(const double2 *__restrict__ a, uint64_t tile0, const int (&hb)[TG_BITS],
                                           int tid, const TileParams &P, double2 *s, double2 (&r)[TRN]) {
   constexpr int NT = 1 << (T - TR);
-  tile_gxfer<false>(const_cast<double2 *>(a), r, tile0, tid, hb);
+  tile_gxfer<T, false>(const_cast<double2 *>(a), r, tile0, tid, hb);
   // current layout: natural (register bits = top TR tile bits, thread bits ascending)
   int cbase = tid, c[TR];
 #pragma unroll
@@ -596,13 +608,13 @@ __device__ __forceinline__ void tile_body(const double2 *__restrict__ a, uint64_
 template <int T>
 __device__ __noinline__ void tile_replay(double2 *__restrict__ a, uint64_t tile0, TileHB h, const TileParams *P,
                                          double2 *s) {
-  int hb[TR];
+  int hb[TG_BITS];
 #pragma unroll
-  for (int k = 0; k < TR; ++k) hb[k] = h.v[k];
+  for (int k = 0; k < TG_BITS; ++k) hb[k] = h.v[k];
   const int tid = threadIdx.x;
   double2 r[TRN];
   tile_body<T, false>(a, tile0, hb, tid, *P, s, r);
-  tile_gxfer<true>(a, r, tile0, tid, hb);
+  tile_gxfer<T, true>(a, r, tile0, tid, hb);
 }
 
 // SPEC = true when the run is mostly diagonal/phase gates (host-chosen):
@@ -613,9 +625,9 @@ template <int T, bool SPEC>
 __global__ void __launch_bounds__(1 << (T - TR), (T <= 12) ? SV_TILE_MINB : 1)
     k_tile(double2 *__restrict__ a, const __grid_constant__ TileParams P) {
   extern __shared__ double2 s[];
-  int hb[TR];
+  int hb[TG_BITS];
 #pragma unroll
-  for (int k = 0; k < TR; ++k) hb[k] = P.hb[k];
+  for (int k = 0; k < TG_BITS; ++k) hb[k] = P.hb[k];
   const uint64_t tile0 = tile_base<T>(blockIdx.x, hb);  // every non-tile slice bit of this CTA
   const int tid = threadIdx.x;
   double2 r[TRN];
@@ -627,12 +639,12 @@ __global__ void __launch_bounds__(1 << (T - TR), (T <= 12) ? SV_TILE_MINB : 1)
     if (__syncthreads_or(!ok)) {
       TileHB h;
 #pragma unroll
-      for (int k = 0; k < TR; ++k) h.v[k] = hb[k];
+      for (int k = 0; k < TG_BITS; ++k) h.v[k] = hb[k];
       tile_replay<T>(a, tile0, h, &P, s);
       return;
     }
   }
-  tile_gxfer<true>(a, r, tile0, tid, hb);
+  tile_gxfer<T, true>(a, r, tile0, tid, hb);
 }
 
 // ------------------------------------------------- same-target stages (exchange)
@@ -1507,13 +1519,13 @@ int classify_kind(const double *q) {
 // Greedy: the register set is the next four distinct targets (padded with the
 // natural bits T-1, T-2, ...); a segment extends while targets stay in it.
 // Returns the number of gates planned (limited by the parameter arrays).
-int plan_tile(const sv_gate *gates, int n, int T, const int (&hb)[TR], TileParams &P) {
+int plan_tile(const sv_gate *gates, int n, int T, const int (&hb)[TG_BITS], TileParams &P) {
   P.nsegs = 0;
-  for (int k = 0; k < TR; ++k) P.hb[k] = hb[k];
+  for (int k = 0; k < TG_BITS; ++k) P.hb[k] = hb[k];
   auto tbit = [&](int g) {  // slice bit -> tile bit, -1 outside the tile
-    if (g < T - TR) return g;
-    for (int k = 0; k < TR; ++k)
-      if (hb[k] == g) return T - TR + k;
+    if (g < T - TG_BITS) return g;
+    for (int k = 0; k < TG_BITS; ++k)
+      if (hb[k] == g) return T - TG_BITS + k;
     return -1;
   };
   int gi = 0;
@@ -1621,7 +1633,7 @@ int launch_tile(double2 *a, int m, int T, const TileParams &P, cudaStream_t st) 
 
 // Run gates (targets in the tile: < T-4 or in hb; controls anywhere) through
 // k_tile, as many launches as the parameter arrays need.
-int run_tile(double2 *a, int m, int T, const int (&hb)[TR], const sv_gate *gates, int n, cudaStream_t st) {
+int run_tile(double2 *a, int m, int T, const int (&hb)[TG_BITS], const sv_gate *gates, int n, cudaStream_t st) {
   static thread_local TileParams P;  // ~20 KB: keep it off the stack
   int off = 0;
   while (off < n) {
@@ -1718,9 +1730,9 @@ int run_mstage(double2 *a, int m, const sv_gate *gates, int n, cudaStream_t st) 
 }
 
 // Native pass planner: the launch group starting at gates[i], returned as its end.
-// Candidate 1, a register-tiled run: targets below L = T-4, or one of up to four
-// higher slice bits taken in order of appearance (the tile then gathers those
-// bits).  Candidate 2, a stage: the run whose targets stay within MS_K = 4
+// Candidate 1, a register-tiled run: targets below L = T-G, or one of up to G
+// (TG_BITS) higher slice bits taken in order of appearance (the tile then
+// gathers those bits).  Candidate 2, a stage: the run whose targets stay within MS_K = 4
 // distinct bits.  Cost model (B200, ms at 2^30 amplitudes, compute overlapping
 // HBM): a pass costs max(5, sum of per-gate costs); per gate, tile 1.15
 // general / 0.45 diagonal (real 0.75, Hadamard-like 0.55), stage by structure (general 0.9, real 0.55,
@@ -1734,13 +1746,13 @@ double stage_cost(const sv_gate &g) {
 }
 
 int next_group(int m, const sv_gate *gates, int n, int i, int T, int *kind) {
-  const int L = T - TR;
+  const int L = T - TG_BITS;
   auto tile_cost = [&](int k) {
     static const double c[KIND_COUNT] = {1.15, 0.45, 0.45, 0.75, 0.55};
     return c[gate_kind(gates[k].q)];
   };
   auto pass = [](double c) { return c > 5.0 ? c : 5.0; };
-  int H[TR], nh = 0, ja = i;
+  int H[TG_BITS], nh = 0, ja = i;
   double ct = 0.0;
   if (T >= 9) {
     for (; ja < n && ja - i < TILE_MAX_GATES; ++ja) {
@@ -1748,7 +1760,7 @@ int next_group(int m, const sv_gate *gates, int n, int i, int T, int *kind) {
       bool in = tt < L;
       for (int k = 0; k < nh && !in; ++k) in = H[k] == tt;
       if (!in) {
-        if (nh == TR) break;
+        if (nh == TG_BITS) break;
         H[nh++] = tt;
       }
       ct += tile_cost(ja);
@@ -1790,23 +1802,23 @@ int exec_group(double2 *a, int m, int T, int kind, const sv_gate *gates, int n, 
     return run_mstage(a, m, gates, n, st);
   }
   if (kind == SV_GROUP_TILE && T >= 9 && n > 1) {
-    const int L = T - TR;
-    int H[TR], nh = 0;
+    const int L = T - TG_BITS;
+    int H[TG_BITS], nh = 0;
     for (int k = 0; k < n; ++k) {
       const int tt = gates[k].target;
       bool in = tt < L;
       for (int q = 0; q < nh && !in; ++q) in = H[q] == tt;
       if (!in) {
-        if (nh == TR) return fail(SV_EINVAL, "tile group: more than %d targets above bit %d", TR, L - 1);
+        if (nh == TG_BITS) return fail(SV_EINVAL, "tile group: more than %d targets above bit %d", TG_BITS, L - 1);
         H[nh++] = tt;
       }
     }
-    for (int b = L; nh < TR; ++b) {  // pad with the natural block bits
+    for (int b = L; nh < TG_BITS; ++b) {  // pad with the natural block bits
       bool dup = false;
       for (int q = 0; q < nh; ++q) dup |= H[q] == b;
       if (!dup) H[nh++] = b;
     }
-    std::sort(H, H + TR);
+    std::sort(H, H + TG_BITS);
     return run_tile(a, m, T, H, gates, n, st);
   }
   for (int k = 0; k < n; ++k) {
@@ -1896,8 +1908,8 @@ int sv_apply_fused(void *amps, int m, int l, const sv_gate *gates, int ngates, v
   // SM overlap one tile's HBM traffic with the other's gates), never below l.
   const int T = l > 12 ? l : (m < 12 ? m : 12);
   if (T >= 9) {
-    int hb[TR];  // contiguous 2^T blocks
-    for (int k = 0; k < TR; ++k) hb[k] = T - TR + k;
+    int hb[TG_BITS];  // contiguous 2^T blocks
+    for (int k = 0; k < TG_BITS; ++k) hb[k] = T - TG_BITS + k;
     return run_tile((double2 *)amps, m, T, hb, gates, ngates, (cudaStream_t)stream);
   }
   static thread_local FusedParams P;  // 18 KB: keep it off the stack

@@ -8,7 +8,7 @@ allow, without reordering any gate:
 * ``local`` pass -- a maximal run of gates with a local target (controls
   anywhere; a control in the rank bits turns into "uncontrolled" or "skip" on
   this rank).  Executed by ``sv_apply_gates``: register-tiled runs for
-  targets below the tile (2^12) plus up to four gathered higher qubits,
+  targets below bit 4 of the tile (2^12) plus up to eight gathered higher qubits,
   multi-target stage passes for runs whose targets lie in at most four qubits
   (four transform stages H(k), R(k, c) for all c are ONE pass), single-gate
   kernels otherwise -- whichever covers the run more cheaply (svb200.cu

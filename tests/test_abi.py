@@ -51,7 +51,7 @@ def test_constants_match_header(lib):
     from paper_1601_07195_b200 import _lib
 
     text = HEADER.read_text()
-    for name in ("SV_FUSED_MAX_TILE", "SV_FUSED_MAX_GATES", "SV_NORM_SCRATCH"):
+    for name in ("SV_FUSED_MAX_TILE", "SV_FUSED_MAX_GATES", "SV_NORM_SCRATCH", "SV_TILE_GATHER"):
         assert int(re.search(rf"#define {name} (\d+)", text).group(1)) == getattr(_lib, name)
     assert lib.sv_version() == _lib.ABI_VERSION
     assert ctypes.sizeof(_lib.SvGate) == 72

@@ -23,15 +23,16 @@ def test_qft_plan_is_one_pass_per_four_stages():
 
 
 def test_random_circuit_plan_fuses_high_targets():
-    """Tiles gather up to four high qubits: random circuits fuse several gates per pass."""
+    """Tiles gather up to SV_TILE_GATHER high qubits: random circuits fuse several gates per pass."""
     circ = sv.random_circuit(30, 400, np.random.default_rng(1), controlled_fraction=0.3)
     plan = sv.plan_passes(circ.gates, 30, 12)
     assert [op for p in plan for op in p.gates] == list(circ.gates)
-    assert len(circ) / len(plan) > 4.0
+    assert len(circ) / len(plan) > 6.0
+    G = sv._lib.SV_TILE_GATHER
     for p in plan:
         if p.kind == "local_tile":
-            high = {op.target for op in p.gates if op.target >= 8}
-            assert len(high) <= 4
+            high = {op.target for op in p.gates if op.target >= 12 - G}
+            assert len(high) <= G
         if p.kind == "local_stage":
             assert len({op.target for op in p.gates}) <= sv._lib.SV_MSTAGE_MAX_TARGETS
 
@@ -54,8 +55,9 @@ def test_plan_is_rank_independent_and_tile_bounds():
         b = sv.plan_passes(list(circ.gates), m, tile_for(12, m))
         assert a == b
         for p in a:
-            if p.kind == "local_tile":  # low bits < T-4 plus at most four gathered high bits
-                assert len({op.target for op in p.gates if op.target >= tile_for(12, m) - 4}) <= 4
+            if p.kind == "local_tile":  # low bits < T-G plus at most G gathered high bits
+                G = sv._lib.SV_TILE_GATHER
+                assert len({op.target for op in p.gates if op.target >= tile_for(12, m) - G}) <= G
             if p.kind == "local_stage":
                 assert len({op.target for op in p.gates}) <= sv._lib.SV_MSTAGE_MAX_TARGETS and len(p.gates) > 1
     assert tile_for(5, 30) == 0 and tile_for(20, 30) == 13 and tile_for(12, 11) == 11
@@ -69,7 +71,7 @@ from hypothesis import strategies as st  # noqa: E402
 @settings(max_examples=60, deadline=None)
 def test_native_planner_invariants(m, seed, tile):
     """sv_plan_gates (the planner sv_apply_gates runs): order-preserving cover, one launch per
-    group, tile groups gather at most four bits above T-4, stages span at most four targets."""
+    group, tile groups gather at most G bits above T-G, stages span at most four targets."""
     rng = np.random.default_rng(seed)
     T = tile if tile and tile <= min(m, 13) else min(m, 13)
     zoo = [sv.hadamard(), sv.phase_r(3), sv.pauli_z(), sv.random_unitary(rng)]
@@ -84,7 +86,8 @@ def test_native_planner_invariants(m, seed, tile):
         targets = {op.target for op in p.gates}
         if p.kind == "local_tile":
             assert len(p.gates) <= sv._lib.SV_FUSED_MAX_GATES
-            assert len({t for t in targets if t >= T - 4}) <= 4
+            G = sv._lib.SV_TILE_GATHER
+            assert len({t for t in targets if t >= T - G}) <= G
         elif p.kind == "local_stage":
             assert len(targets) <= sv._lib.SV_MSTAGE_MAX_TARGETS and 1 < len(p.gates) <= sv._lib.SV_MSTAGE_MAX_GATES
         else:
