@@ -75,6 +75,37 @@ def test_tile_runs_bitwise(n, T):
         assert bits_equal(a.cpu().numpy(), run_oracle(v, ops)), (n, T, trial)
 
 
+@pytest.mark.parametrize("T", [9, 10, 12, 13])
+def test_gathered_tile_groups_bitwise(T):
+    """Forced SV_GROUP_TILE groups whose targets are SV_TILE_GATHER high slice bits spread over
+    the whole slice (top bit included) plus the contiguous low bits; controls on register,
+    thread (warp and lane) and above-tile bits.  Bitwise vs the oracle."""
+    from paper_1601_07195_b200 import _lib
+    from paper_1601_07195_b200.kernels import device_view, gate_array, stream_handle
+
+    n, G = 20, sv._lib.SV_TILE_GATHER
+    rng = np.random.default_rng(77 + T)
+    for trial in range(3):
+        high = sorted(int(x) for x in rng.choice(np.arange(T - G, n), G, replace=False))
+        if trial == 0:
+            high[-1] = n - 1
+        tset = list(range(T - G)) + high
+        ops = []
+        for _ in range(150):
+            t = tset[int(rng.integers(len(tset)))]
+            c = None if rng.random() < 0.4 else int(rng.integers(n - 1))
+            c = None if c is None else (c + 1 if c >= t else c)
+            g = gate_zoo(rng)[int(rng.integers(10))] if rng.random() < 0.5 else sv.random_unitary(rng)
+            ops.append(sv.GateOp(g, t, c))
+        v = with_zeros(rng, n) if trial else random_state(rng, n)
+        a = torch.from_numpy(v.copy()).to(DEV)
+        ptr, m = device_view(a)
+        assert _lib.load().sv_apply_group(ptr, m, _lib.SV_GROUP_TILE, gate_array(ops), len(ops), T,
+                                          stream_handle()) == 0, _lib.load().sv_last_error()
+        torch.cuda.synchronize()
+        assert bits_equal(a.cpu().numpy(), run_oracle(v, ops)), (T, trial, high)
+
+
 def test_tile_register_set_transitions_and_natural_layout():
     """Target sequences that hit the natural layout, force many transposes, or repeat one target."""
     n = 14
