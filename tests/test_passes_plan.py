@@ -13,11 +13,11 @@ def test_qft_plan_is_one_pass_per_four_stages():
     circ = sv.build_qft(n)
     plan = sv.plan_passes(circ.gates, m, 12)
     # four consecutive transform stages H(k), R(k, c) for all c < k share one stage pass; the
-    # last two (targets 0..1, strided for a stage) go through the register tile
+    # last six (targets 0..5: a strided stage plus a leftover pass otherwise) are one register tile
     assert sv._lib.SV_MSTAGE_MAX_TARGETS == 4
-    assert [p.kind for p in plan] == ["local_stage"] * 7 + ["local_tile"]
+    assert [p.kind for p in plan] == ["local_stage"] * 6 + ["local_tile"]
     assert [sorted({op.target for op in p.gates}) for p in plan] == (
-        [[k - 3, k - 2, k - 1, k] for k in range(29, 2, -4)] + [[0, 1]])
+        [[k - 3, k - 2, k - 1, k] for k in range(29, 6, -4)] + [list(range(6))])
     assert [op for p in plan for op in p.gates] == list(circ.gates)
     assert max(len(p.gates) for p in plan) <= sv._lib.SV_MSTAGE_MAX_GATES
 
