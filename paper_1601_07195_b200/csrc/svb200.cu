@@ -636,7 +636,11 @@ __device__ __noinline__ void tile_replay(double2 *__restrict__ a, uint64_t tile0
 // zero component the whole tile is replayed exactly from global memory
 // (nothing has been stored yet).  SPEC = false: the exact path.
 template <int T, bool SPEC>
-__global__ void __launch_bounds__(1 << (T - TR), (T <= 12) ? SV_TILE_MINB : 1)
+#ifndef SV_TILE_THREADS_SM
+#define SV_TILE_THREADS_SM 512  // resident threads per SM the register budget must allow (0: SV_TILE_MINB CTAs); T = 11 at
+// 512 (4 CTAs) instead of 256 (2): random 25-gate steps 32.1 -> 26.7 ms; 768 (80 registers) spills and is slower
+#endif
+__global__ void __launch_bounds__(1 << (T - TR), (T <= 12) ? (SV_TILE_THREADS_SM ? SV_TILE_THREADS_SM / (1 << (T - TR)) : SV_TILE_MINB) : 1)
     k_tile(double2 *__restrict__ a, const __grid_constant__ TileParams P) {
   extern __shared__ double2 s[];
   int hb[TG_BITS];

@@ -58,7 +58,7 @@ def main():
         "tile_qft12_ms": timed(lambda: sv.kernels.apply_gates(st.amps, diag, tile=12), reps),
         "qft_ms": timed(lambda: sv.run_circuit(st, qft, fusion=fc), reps),
     }
-    for lc in (12, 11):
+    for lc in (12, 11, 10):
         steps = [[sv.GateOp(sv.random_unitary(rng), int(rng.integers(n))) for _ in range(25)] for _ in range(4)]
         fl = sv.FusionConfig(l_c=lc, passes=True)
         res[f"random25_lc{lc}_ms"] = timed(lambda: [sv.run_circuit(st, sv.Circuit(n, g), fusion=fl) for g in steps], reps) / 4
@@ -69,9 +69,12 @@ def main():
             c, t = (int(x) for x in rng.choice(n, 2, replace=False))
             ops.append(sv.GateOp(sv.random_unitary(rng), t, c))
         csteps.append(ops)
-    fl = sv.FusionConfig(l_c=12, passes=True)
-    res["controlled25_lc12_ms"] = timed(lambda: [sv.run_circuit(st, sv.Circuit(n, g), fusion=fl) for g in csteps],
-                                        reps) / 4
+    for lc in (12, 11):
+        fl = sv.FusionConfig(l_c=lc, passes=True)
+        res[f"controlled25_lc{lc}_ms"] = timed(
+            lambda: [sv.run_circuit(st, sv.Circuit(n, g), fusion=fl) for g in csteps], reps) / 4
+    f11 = sv.FusionConfig(l_c=11, passes=True)
+    res["qft_lc11_ms"] = timed(lambda: sv.run_circuit(st, qft, fusion=f11), reps)
     b = sv.init_basis_state(sv.Layout(n), 5)
     res["qft_basis_ms"] = timed(lambda: sv.run_circuit(b, qft, fusion=fc), 1)
     print(json.dumps(res))
