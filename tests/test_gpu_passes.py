@@ -106,6 +106,28 @@ def test_gathered_tile_groups_bitwise(T):
         assert bits_equal(a.cpu().numpy(), run_oracle(v, ops)), (T, trial, high)
 
 
+def test_tile_group_rejects_too_many_gathered_bits():
+    """A forced tile group with SV_TILE_GATHER + 1 distinct targets above the contiguous bits is
+    refused (SV_EINVAL, state untouched), exactly G is accepted."""
+    from paper_1601_07195_b200 import _lib
+    from paper_1601_07195_b200.kernels import device_view, gate_array, stream_handle
+
+    n, T, G = 20, 12, sv._lib.SV_TILE_GATHER
+    v = random_state(np.random.default_rng(3), n)
+    a = torch.from_numpy(v.copy()).to(DEV)
+    ptr, m = device_view(a)
+    L = _lib.load()
+    too_many = [sv.GateOp(sv.hadamard(), t) for t in range(T - G, T - G + G + 1)]
+    assert L.sv_apply_group(ptr, m, _lib.SV_GROUP_TILE, gate_array(too_many), len(too_many), T,
+                            stream_handle()) == _lib.SV_EINVAL
+    torch.cuda.synchronize()
+    assert bits_equal(a.cpu().numpy(), v)
+    ok = too_many[:G]
+    assert L.sv_apply_group(ptr, m, _lib.SV_GROUP_TILE, gate_array(ok), len(ok), T, stream_handle()) == 0
+    torch.cuda.synchronize()
+    assert bits_equal(a.cpu().numpy(), run_oracle(v, ok))
+
+
 def test_tile_register_set_transitions_and_natural_layout():
     """Target sequences that hit the natural layout, force many transposes, or repeat one target."""
     n = 14
