@@ -8,14 +8,21 @@ k = 0..n-1 in order (at N > 1 the top log2(N) targets are global qubits and
 run the fused NVLink exchange).  Weak scaling: per-GPU work is fixed.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload sweep|controlled|random|qft] [--n N]
+                    [--workload sweep|controlled|random|qft] [--qubits N]
 
-Prints ONE JSON line on rank 0.  `value` is the effective HBM bandwidth per
-gate of the whole job, (gates x 32 x 2^n bytes) / time, the paper's
+``--gpus N`` without torchrun launches N ranks itself (torch.distributed.run,
+127.0.0.1); under torchrun WORLD_SIZE must equal N.  Prints ONE JSON line on
+rank 0.  `value` is the effective HBM bandwidth per gate of the whole job,
+(gates x 32 x 2^n bytes) / time (16 x 2^n for controlled gates), the paper's
 "effective GB/s per gate"; `gates_per_s` rides along.
 Timing: W untimed steps, then K steps between barrier+synchronize, CUDA
 events on the launching stream, max over ranks.  The 16 GiB slice is ~130x
 the 126 MB L2, so no flush is needed between steps.
+
+The same line carries the BASELINE configs 3 / 4 / 5 shapes as secondary
+objects (``secondary``: config-3 controlled gates per gate with (c, t) buckets,
+config-4-shaped random steps and the config-5 transform through the pass
+planner, exact and tolerance-mode), each with its own roofline.
 """
 
 from __future__ import annotations
@@ -23,6 +30,8 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
+import subprocess
 import sys
 import threading
 import time
@@ -36,21 +45,23 @@ sys.path.insert(0, str(ROOT))
 METRIC = "gates/sec & effective HBM GB/s per gate vs 8 TB/s at n qubits; 1/2/4/8 GPU"
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--gpus", type=int, default=None,
+                    help="GPUs (ranks) of the job; default WORLD_SIZE under torchrun, else 1")
     ap.add_argument("--steps", type=int, default=10, help="timed steps (BASELINE config 2: 10 repetitions of the sweep)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=["sweep", "controlled", "random", "qft"], default="sweep")
     ap.add_argument("--qubits", dest="n", type=int, default=None, help="total qubits (default 30 + log2(N))")
-    ap.add_argument("--fusion", choices=["none", "passes"], default=None,
+    ap.add_argument("--fusion", choices=["none", "passes", "tolerance"], default=None,
                     help="none: one launch per gate (default, BASELINE config 2 is per-gate); "
-                         "passes: native pass planner (default for --workload qft)")
+                         "passes: native pass planner, bitwise (default for --workload qft); "
+                         "tolerance: passes with exact=False (collapsed diagonals, 1e-12*sqrt(G) parity)")
     ap.add_argument("--l-c", type=int, default=12, help="register tile exponent for --fusion passes")
-    ap.add_argument("--data-plane", choices=["ipc", "nccl"], default="ipc",
-                    help="global-qubit exchanges: fused kernel on CUDA-IPC-mapped peer slices (default) or the "
-                         "reference's staged pipeline over NCCL send/recv (baseline)")
+    ap.add_argument("--data-plane", choices=["ipc", "nccl", "ce"], default="ipc",
+                    help="global-qubit exchanges: fused kernel on CUDA-IPC-mapped peer slices (default), the "
+                         "reference's staged pipeline over NCCL send/recv (baseline) or copy-engine chunks")
     ap.add_argument("--diagonal-local", action="store_true",
                     help="diagonal gates on global qubits without an exchange (SURVEY.md 8(f)1; off by default: "
                          "it departs from the reference's per-gate NVLink traffic contract)")
@@ -58,9 +69,11 @@ def parse():
                     help="global<->local qubit swaps instead of per-gate exchanges (SURVEY.md 8(f)4; N > 1)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the config 3/4/5 secondary objects")
+    ap.add_argument("--planes", action="store_true", help="N > 1: also time every exchange data plane")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--out", default=None, help="also write the JSON line here")
-    return ap.parse_args()
+    return ap.parse_args(argv)
 
 
 def dist_env():
@@ -68,6 +81,39 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return world, rank, local
+
+
+def job_size(args, env=None) -> int:
+    """Number of ranks of the job.  Under torchrun WORLD_SIZE decides and --gpus must agree;
+    without it, --gpus (default 1)."""
+    env = os.environ if env is None else env
+    if "WORLD_SIZE" in env:
+        world = int(env["WORLD_SIZE"])
+        if args.gpus is not None and args.gpus != world:
+            raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU "
+                             f"(torchrun --nproc-per-node {args.gpus}) or drop --gpus")
+        n = world
+    else:
+        n = args.gpus or 1
+    if n < 1 or n & (n - 1):
+        raise SystemExit(f"bench.py: --gpus must be a power of two, got {n}")
+    return n
+
+
+def launch_command(args, argv, port: int) -> list[str] | None:
+    """The torch.distributed.run command that fans --gpus N out to N ranks (one per GPU),
+    or None when this process already is a rank / the job has one rank (the reference's
+    run_spmd rank fan-out, pkg/src/svsim/transport.py:274-310)."""
+    if "WORLD_SIZE" in os.environ or (args.gpus or 1) == 1:
+        return None
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+            "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()), *argv]
+
+
+def free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
 
 
 def step_circuits(sv, workload, n, count, seed=1):
@@ -164,9 +210,11 @@ def ncu_traffic(kernel_key, alg_bytes):
     try:
         d = json.loads((ROOT / "profiles" / "ncu_summary.json").read_text())["kernels"][kernel_key]
         scale = alg_bytes / d.get("algorithmic_bytes", alg_bytes)
-        return round(d["dram_bytes_per_launch"] * scale)
+        out = {"dram_bytes_per_launch": round(d["dram_bytes_per_launch"] * scale),
+               "captured_at_m": d.get("m"), "source": "profiles/ncu_summary.json"}
+        return out["dram_bytes_per_launch"], out
     except (OSError, KeyError, ValueError, TypeError):
-        return None
+        return None, None
 
 
 def cpu_baseline(sv, host_state, n, circ, seconds):
@@ -192,52 +240,127 @@ def cpu_baseline(sv, host_state, n, circ, seconds):
                       f"OpenMP threads, {dt:.2f} s"}
 
 
-def run_reference(args):
-    """--impl reference: the reference's CPU algorithm (oracle port, all host threads) on our config."""
-    world, rank, _ = dist_env()
+# ------------------------------------------------------------------ reference arm
+
+
+def rank_share(oracle, amps, partner, op, m, rep_rank, threads):
+    """One representative rank's share of one gate on the CPU port (oracle/sv_oracle.c):
+    local gates on its 2^m slice, global targets as its half of the pairwise exchange
+    against a second host slice standing in for the partner (distributed.py:187-422)."""
+    t, c = op.target, op.control
+    if t < m and (c is None or c < m):
+        oracle.apply_gate(amps, op, threads=threads)
+        return
+    if t < m:  # control on a rank bit: the representative rank has it set
+        oracle.apply_single(amps, t, op.gate, threads=threads)
+        return
+    own_zero = ((rep_rank >> (t - m)) & 1) == 0
+    oracle.exchange(amps, partner, own_zero, -1 if c is None or c >= m else c, op.gate, threads=threads)
+
+
+def stock_reference(n, circ, seconds):
+    """The stock reference (baseline/_ref: svsim installed unmodified from /root/reference) through
+    its public API, svsim.run_circuit(..., policy=ThreadPolicy(os.cpu_count())), on a bounded
+    sample of the step's gates on a 2^n host state (engine.py:30-96, kernels.py:83-105)."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "svsim").exists():
+        return {"unavailable": "baseline/_ref/svsim not installed"}
+    sys.path.insert(0, str(ref))
+    try:
+        import svsim
+        from svsim.kernels import ThreadPolicy
+    except Exception as exc:  # noqa: BLE001
+        return {"unavailable": f"import svsim failed: {exc!r}"}
+    finally:
+        sys.path.remove(str(ref))
+    threads = os.cpu_count() or 1
+    from oracle import oracle
+
+    amps = np.empty(1 << n, dtype=np.complex128)
+    oracle.fill_philox(amps, 0, 0, threads)
+    state = svsim.LocalState(svsim.Layout(n, 0, 0), amps)
+    policy = ThreadPolicy(threads)
+    done, nbytes, t_all = 0, 0, 0.0
+    for op in circ:
+        one = svsim.Circuit(n, [svsim.GateOp(svsim.GateMatrix(op.gate.mat), op.target, op.control)])
+        t0 = time.perf_counter()
+        svsim.run_circuit(state, one, policy=policy)
+        t_all += time.perf_counter() - t0
+        done += 1
+        nbytes += (32 if op.control is None else 16) << n
+        if t_all > seconds:
+            break
+    return {"value": round(nbytes / t_all / 1e9, 3), "unit": "GB/s", "cores": threads, "kind": "reference",
+            "gates": done, "seconds": round(t_all, 3),
+            "sample": f"first {done} gates of the step, svsim.run_circuit(policy=ThreadPolicy({threads})) "
+                      f"from baseline/_ref on a 2^{n} host state"}
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the reference's CPU algorithm on our config, rank 0 only.
+
+    Timed: the oracle port (oracle/sv_oracle.c, the reference's arithmetic restated in C,
+    OpenMP on every host thread) running the GPU arm's step circuits (same seeds, same
+    per-step gates) on the same seeded state recipe.  At N = 1 each timed step is the whole
+    step circuit (same_config).  At N > 1 the whole 2^n state does not fit one host: each step
+    times one representative rank's share (every rank bit set, so every control-set rank's
+    work is done) on a 2^m slice plus a partner slice, and the whole job is N such shares
+    run back to back on the one host (the CPU path is memory-bound).  The stock reference
+    (svsim from baseline/_ref) is timed beside it on a bounded sample (``stock_reference``)."""
     if rank != 0:
         return
-    import paper_1601_07195_b200 as sv
+    import paper_1601_07195_b200 as sv  # circuits only (the reference's RNG order), no kernels
     from oracle import oracle
 
     g = world.bit_length() - 1
     n = args.n or (30 + g)
     m = n - g
+    rep = world - 1
     threads = os.cpu_count() or 1
-    # One host holds one rank's 2^m slice (16 GiB at the default size): the CPU
-    # path is memory-bound, so the whole job on one host runs each gate's
-    # per-rank shares back to back and whole-job GB/s equals the slice rate.
     amps = np.empty(1 << m, dtype=np.complex128)
-    oracle.fill_phase(amps, threads)
-    pool = [op for op in step_circuits(sv, args.workload, n, 1)[0].gates if op.max_qubit() < m]
+    oracle.fill_philox(amps, 0, rep, threads)
+    partner = None
+    if g:
+        partner = np.empty(1 << m, dtype=np.complex128)
+        oracle.fill_philox(partner, 0, rep ^ 1, threads)
+    circs = step_circuits(sv, args.workload, n, args.warmup + args.steps)
     times, eff = [], 0
-    for s in range(args.warmup + args.steps):
-        op = pool[(s * 7) % len(pool)]
+    for s, circ in enumerate(circs):
+        ops = circ.gates if s >= args.warmup else circ.gates[:1]  # warm-up: page in, spin up threads
         t0 = time.perf_counter()
-        oracle.apply_gate(amps, op, threads=threads)
+        for op in ops:
+            rank_share(oracle, amps, partner, op, m, rep, threads)
         dt = time.perf_counter() - t0
         if s >= args.warmup:
-            times.append(dt)
-            eff += (32 if op.control is None else 16) << m
+            times.append(dt * world)
+            eff += effective_bytes(circ, n)
     tot = sum(times)
     value = eff / tot / 1e9
+    stock = stock_reference(min(n, 30), circs[-1].gates if args.workload != "qft" else circs[-1].gates[:3],
+                            args.cpu_seconds) if not args.no_cpu_baseline else None
+    sample = (f"every gate of each of the {args.steps} step circuits on the seeded 2^{n} state" if g == 0 else
+              f"rank {rep}'s share of every gate of each of the {args.steps} step circuits on a 2^{m} slice "
+              f"(+ a partner slice for exchanges), x {world} ranks back to back on this host")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(tot / args.steps * 1e3, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-        "gates_per_s": round(args.steps / tot, 4),
+        "gates_per_s": round(sum(len(c) for c in circs[args.warmup:]) / tot, 4),
         "config": {"workload": WORKLOADS[args.workload].format(n=n, n1=n - 1), "n_qubits": n, "local_qubits": m,
-                   "sample": f"one local gate of the step per timed step (target 7*s mod len), on one "
-                             f"2^{m}-amplitude rank slice"},
+                   "global_qubits": g, "gates_per_step": len(circs[-1]), "seed": {"state": 0, "circuit": 1},
+                   "same_config": g == 0, "sample": sample},
         "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": threads, "kind": "port",
-                         "sample": f"{args.steps} gates of the step on a 2^{m}-amplitude host slice, "
-                                   f"oracle/sv_oracle.c (C restatement of kernels.py:120-196), {threads} threads"},
+                         "sample": f"{sample}; oracle/sv_oracle.c (C restatement of kernels.py:120-196, "
+                                   f"distributed.py:187-202), {threads} OpenMP threads"},
+        "stock_reference": stock,
         "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     if args.out:
         Path(args.out).write_text(json.dumps(line) + "\n")
 
+
+# ------------------------------------------------------------------ GPU arm
 
 # FP64 pipe ops per pair of the cheapest exact update each gate shape admits (svb200.cu spec_pair):
 # general mix() 20, real 12, Hadamard-like 8, diagonal 8, phase 4 (one cmul on the |1> side).
@@ -272,7 +395,7 @@ def p2p_probe(state, fabric, dev, barrier, reduce_scalar, nbytes=1 << 31, reps=3
     import torch.distributed as dist
 
     fabric.ensure_registered(state)
-    if fabric.data_plane != "ipc":
+    if fabric.data_plane == "nccl":
         return None
     nbytes = min(nbytes, 16 << state.layout.m)
     src = fabric.peer_pointer(state, fabric.rank ^ 1)
@@ -308,13 +431,14 @@ def make_units(sv, circ, m, fusion, l_c, state, fabric, remap=False):
             else:
                 units += make_units(sv, sv.Circuit(circ.n, it), m, fusion, l_c, state, fabric)
         return units
-    if fusion == "passes":
+    if fusion in ("passes", "tolerance"):
         from paper_1601_07195_b200.passes import tile_for
 
         tile = tile_for(l_c, m)
+        exact = fusion == "passes"
         return [("pass-" + p.kind, (32 << m) if p.local else (1 << (m + 4)), len(p.gates),
                  (lambda p=p: sv.execute_pass(state, p, fabric, tile=tile)), p.gates)
-                for p in sv.plan_passes(circ.gates, m, tile)]
+                for p in sv.plan_passes(circ.gates, m, tile, exact=exact)]
     units = []
     for op in circ:
         case = sv.classify_case(op.target, op.control, m)
@@ -336,25 +460,128 @@ KERNELS = {
     "pass-local_stage": ("sv_apply_gates:stage", "k_mstage (sv_apply_gates, multi-target stage pass)"),
     "pass-local_tile": ("sv_apply_gates:tile", "k_tile (sv_apply_gates, register-tiled run)"),
     "pass-local_gate": ("sv_apply_single", "k_pairs/k_shfl (single gate of a pass plan)"),
+    "pass-local_diag": ("sv_apply_gates:diag", "k_dstage (tolerance mode: collapsed diagonal stages)"),
 }
+GLOBAL_KINDS = ("exchange", "swap", "pass-global_stage", "pass-global_gate")
 
 
-def main():
-    args = parse()
-    if args.impl == "reference":
-        run_reference(args)
-        return
+class Timer:
+    """Runs step circuits unit by unit with CUDA events on the launching stream."""
+
+    def __init__(self, sv, torch, dist, world, stream, barrier, reduce_scalar, local):
+        self.sv, self.torch, self.dist, self.world = sv, torch, dist, world
+        self.stream, self.barrier, self.reduce_scalar, self.local = stream, barrier, reduce_scalar, local
+
+    def run(self, circs, state, m, fabric, fusion, l_c, remap=False):
+        torch, sv = self.torch, self.sv
+        units = [make_units(sv, c, m, fusion, l_c, state, fabric, remap) for c in circs]
+        ev = []
+        launches0 = sv.launch_count()
+        with ClockSampler(self.local) as clocks:
+            self.barrier()
+            t0 = torch.cuda.Event(enable_timing=True)
+            t1 = torch.cuda.Event(enable_timing=True)
+            t0.record(self.stream)
+            for us in units:
+                row = [torch.cuda.Event(enable_timing=True)]
+                row[0].record(self.stream)
+                for _, _, _, fn, _ in us:
+                    fn()
+                    e = torch.cuda.Event(enable_timing=True)
+                    e.record(self.stream)
+                    row.append(e)
+                ev.append(row)
+            t1.record(self.stream)
+            torch.cuda.synchronize()
+        launches = sv.launch_count() - launches0
+        elapsed = t0.elapsed_time(t1)
+        if self.world > 1:
+            elapsed = self.reduce_scalar(elapsed, self.dist.ReduceOp.MAX)
+            launches = int(self.reduce_scalar(float(launches), self.dist.ReduceOp.SUM))
+        unit_ms = [[row[i].elapsed_time(row[i + 1]) for i in range(len(row) - 1)] for row in ev]
+        return {"elapsed_ms": elapsed, "unit_ms": unit_ms, "units": units, "launches": launches,
+                "clocks": clocks.summary()}
+
+
+def roofline(res, m, peaks, peak_kind):
+    """Roofline of the dominant local kernel (largest share of the timed region)."""
+    by_kind: dict = {}
+    for us, ms in zip(res["units"], res["unit_ms"]):
+        for (kind, nbytes, cnt, _, gates), t_ms in zip(us, ms):
+            by_kind.setdefault(kind, []).append((nbytes, t_ms, cnt, gates))
+    local_kinds = [k for k in by_kind if k in KERNELS]
+    if not local_kinds:
+        return None, by_kind
+    top = max(local_kinds, key=lambda k: sum(r[1] for r in by_kind[k]))
+    rows = by_kind[top]
+    avg_ms = float(np.mean([r[1] for r in rows]))
+    alg = int(np.mean([r[0] for r in rows]))
+    achieved = alg / (avg_ms * 1e-3) / 1e9
+    key, kname = KERNELS[top]
+    traffic, tsrc = ncu_traffic(key, alg)
+    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+            "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": traffic, "traffic_source": tsrc,
+            "kernel": kname, "peak_kind": peak_kind, "algorithmic_bytes_per_launch": alg,
+            "avg_launch_ms": round(avg_ms, 4), "launches": len(rows),
+            "share_of_step": round(sum(r[1] for r in rows) / res["elapsed_ms"], 4),
+            "frac_of_8TBs": round(achieved / 8000.0, 4)}
+    if top.startswith("pass-"):
+        roof["gates_per_launch"] = round(float(np.mean([r[2] for r in rows])), 2)
+        # fused passes are FP64-pipe bound once a pass carries enough gates: report that roofline too
+        ops = float(np.mean([fp64_ops(r[3], m) for r in rows]))
+        roof["fp64"] = {"achieved_tops": round(ops / (avg_ms * 1e-3) / 1e12, 3),
+                        "peak_tops": FP64_PEAK_OPS / 1e12, "frac": round(ops / (avg_ms * 1e-3) / FP64_PEAK_OPS, 4),
+                        "ops_per_launch": int(ops), "peak_kind": "measured (tools/micro/fp64_probe.cu)",
+                        "note": "exact-update op counts; tolerance-mode collapsed diagonals do fewer"}
+    return roof, by_kind
+
+
+def controlled_buckets(circs, unit_ms, m):
+    """GB/s (16*2^m accounting) by c<t / c>t and by min(c,t) / c."""
+    buckets = {}
+    for c_circ, ms in zip(circs, unit_ms):
+        for op, t_ms in zip(c_circ, ms):
+            if op.control is None or op.max_qubit() >= m:
+                continue
+            lo = min(op.control, op.target)
+            band = "0" if lo == 0 else "1" if lo == 1 else "2-4" if lo <= 4 else ">=5"
+            cb = str(op.control) if op.control <= 2 else ">=3"
+            for key in (f"c<t" if op.control < op.target else "c>t", f"min(c,t)={band}", f"c={cb}"):
+                buckets.setdefault(key, []).append(t_ms)
+    return {k: {"gbps": round((16 << m) / (float(np.median(v)) * 1e-3) / 1e9, 1), "gates": len(v)}
+            for k, v in sorted(buckets.items())}
+
+
+def probe_and_exit(world, rank, n, m):
+    """SVB_BENCH_PROBE=1: report the rank layout the launcher produced, then stop (CPU tests)."""
+    print(json.dumps({"probe": True, "rank": rank, "world": world, "n_qubits": n, "local_qubits": m,
+                      "global_qubits": n - m}), flush=True)
+
+
+def run_ours(args, world, rank, local):
     import torch
     import torch.distributed as dist
 
+    g = world.bit_length() - 1
+    n = args.n or (30 + g)
+    if os.environ.get("SVB_BENCH_PROBE") == "1":
+        if world > 1:
+            dist.init_process_group("gloo")
+            dist.barrier()
+        probe_and_exit(world, rank, n, n - g)
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
     import paper_1601_07195_b200 as sv
 
-    world, rank, local = dist_env()
     # SVB_SHARE_DEVICE=1 (diagnostics only): every rank on cuda:0 over gloo with host fences,
     # to exercise the multi-rank bench path on a one-GPU box.  Never used for reported numbers.
     shared = os.environ.get("SVB_SHARE_DEVICE") == "1"
     if shared:
         local = 0
+    elif world > torch.cuda.device_count():
+        raise SystemExit(f"bench.py: {world} ranks but only {torch.cuda.device_count()} visible GPU(s)")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     fabric = None
@@ -364,10 +591,6 @@ def main():
         else:
             dist.init_process_group("nccl", device_id=dev)
         fabric = sv.NvlinkFabric(data_plane=args.data_plane, diagonal_local=args.diagonal_local)
-    if world & (world - 1):
-        raise SystemExit("--gpus must be a power of two")
-    g = world.bit_length() - 1
-    n = args.n or (30 + g)
     lay = sv.Layout(n, g, rank)
     m = lay.m
     fusion = args.fusion or ("passes" if args.workload == "qft" else "none")
@@ -377,7 +600,14 @@ def main():
     free_b, _ = torch.cuda.mem_get_info(dev)
     initial = state.amps.clone() if free_b > 5 * (16 << lay.m) else None
     stream = torch.cuda.current_stream()
-    fcfg = sv.FusionConfig(l_c=args.l_c, passes=True) if fusion == "passes" else None
+    applied = []  # (circuit, FusionConfig) in order, for the self-check
+
+    def fcfg_of(f):
+        if f == "passes":
+            return sv.FusionConfig(l_c=args.l_c, passes=True)
+        if f == "tolerance":
+            return sv.FusionConfig(l_c=args.l_c, passes=True, exact=False)
+        return None
 
     def barrier():
         torch.cuda.synchronize()
@@ -389,10 +619,14 @@ def main():
         dist.all_reduce(t, op=op)
         return float(t[0])
 
+    timer = Timer(sv, torch, dist, world, stream, barrier, reduce_scalar, local)
+    peaks, peak_kind = load_peaks()
+
     # ---------------------------------------------------------- warm-up
     for c in circs[: args.warmup]:
         for _, _, _, fn, _ in make_units(sv, c, m, fusion, args.l_c, state, fabric, args.remap):
             fn()
+        applied.append((c, fcfg_of(fusion)))
     barrier()
 
     # ------------------------- NVLink reference: copy-engine peer read, all pairs at once
@@ -400,107 +634,79 @@ def main():
 
     # ------------------------------------------------ timed (device-resident)
     timed = circs[args.warmup:]
-    units = [make_units(sv, c, m, fusion, args.l_c, state, fabric, args.remap) for c in timed]
-    ev = []
-    launches0 = sv.launch_count()
-    with ClockSampler(local) as clocks:
-        barrier()
-        t_start = torch.cuda.Event(enable_timing=True)
-        t_end = torch.cuda.Event(enable_timing=True)
-        t_start.record(stream)
-        for us in units:
-            row = [torch.cuda.Event(enable_timing=True)]
-            row[0].record(stream)
-            for _, _, _, fn, _ in us:
-                fn()
-                e = torch.cuda.Event(enable_timing=True)
-                e.record(stream)
-                row.append(e)
-            ev.append(row)
-        t_end.record(stream)
-        torch.cuda.synchronize()
-    launches = sv.launch_count() - launches0
-    elapsed_ms = t_start.elapsed_time(t_end)
-    if world > 1:
-        elapsed_ms = reduce_scalar(elapsed_ms, dist.ReduceOp.MAX)
-        launches = int(reduce_scalar(float(launches), dist.ReduceOp.SUM))
-    unit_ms = [[row[i].elapsed_time(row[i + 1]) for i in range(len(row) - 1)] for row in ev]
+    res = timer.run(timed, state, m, fabric, fusion, args.l_c, args.remap)
+    applied += [(c, fcfg_of(fusion)) for c in timed]
+    elapsed_ms = res["elapsed_ms"]
     ngates = sum(len(c) for c in timed)
     eff = sum(effective_bytes(c, n) for c in timed)
     value = eff / (elapsed_ms * 1e-3) / 1e9
-
-    # roofline of the dominant local kernel (largest share of the step)
-    peaks, peak_kind = load_peaks()
-    by_kind: dict = {}
-    for us, ms in zip(units, unit_ms):
-        for (kind, nbytes, cnt, _, gates), t_ms in zip(us, ms):
-            by_kind.setdefault(kind, []).append((nbytes, t_ms, cnt, gates))
-    local_kinds = [k for k in by_kind if k in KERNELS]
-    roof = None
-    if local_kinds:
-        top = max(local_kinds, key=lambda k: sum(r[1] for r in by_kind[k]))
-        rows = by_kind[top]
-        avg_ms = float(np.mean([r[1] for r in rows]))
-        alg = int(np.mean([r[0] for r in rows]))
-        achieved = alg / (avg_ms * 1e-3) / 1e9
-        key, kname = KERNELS[top]
-        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": ncu_traffic(key, alg),
-                "kernel": kname, "peak_kind": peak_kind, "algorithmic_bytes_per_launch": alg,
-                "avg_launch_ms": round(avg_ms, 4), "launches": len(rows),
-                "share_of_step": round(sum(r[1] for r in rows) / elapsed_ms, 4),
-                "frac_of_8TBs": round(achieved / 8000.0, 4)}
-        if top.startswith("pass-"):
-            roof["gates_per_launch"] = round(float(np.mean([r[2] for r in rows])), 2)
-            # fused passes are FP64-pipe bound once a pass carries enough gates: report that roofline too
-            ops = float(np.mean([fp64_ops(r[3], m) for r in rows]))
-            roof["fp64"] = {"achieved_tops": round(ops / (avg_ms * 1e-3) / 1e12, 3),
-                            "peak_tops": FP64_PEAK_OPS / 1e12, "frac": round(ops / (avg_ms * 1e-3) / FP64_PEAK_OPS, 4),
-                            "ops_per_launch": int(ops), "peak_kind": "measured (tools/micro/fp64_probe.cu)"}
+    roof, by_kind = roofline(res, m, peaks, peak_kind)
     per_target = {}
     if args.workload == "sweep" and fusion == "none":
         for k in range(m):
-            ks = [unit_ms[j][k] for j in range(len(timed))]
+            ks = [res["unit_ms"][j][k] for j in range(len(timed))]
             per_target[k] = round((32 << m) / (float(np.median(ks)) * 1e-3) / 1e9, 1)
-    buckets = {}
-    if args.workload == "controlled" and fusion == "none":
-        # GB/s (16*2^m accounting) by c<t / c>t and by min(c,t)
-        for c_circ, ms in zip(timed, unit_ms):
-            for op, t_ms in zip(c_circ, ms):
-                if op.control is None or op.max_qubit() >= m:
-                    continue
-                lo = min(op.control, op.target)
-                band = "0" if lo == 0 else "1" if lo == 1 else "2-4" if lo <= 4 else ">=5"
-                for key in (f"c<t" if op.control < op.target else "c>t", f"min(c,t)={band}"):
-                    buckets.setdefault(key, []).append(t_ms)
-        buckets = {k: {"gbps": round((16 << m) / (float(np.median(v)) * 1e-3) / 1e9, 1), "gates": len(v)}
-                   for k, v in sorted(buckets.items())}
-    nvlink = None
-    glob = [r for k, rs in by_kind.items() if k in ("exchange", "swap", "pass-global_stage", "pass-global_gate")
-            for r in rs]
-    if world > 1 and glob:
-        d = float(np.mean([r[1] for r in glob]))
-        ach = sum(r[0] for r in glob) / (sum(r[1] for r in glob) * 1e-3) / 1e9  # link bytes per direction / time
-        nvlink = {"achieved_gbs_per_direction": round(ach, 1),
-                  "peak_nominal": 900.0, "peak_measured_p2p": p2p["gbs_per_direction"] if p2p else None,
-                  "frac_nominal": round(ach / 900.0, 4),
-                  "frac_measured": round(ach / p2p["gbs_per_direction"], 4) if p2p else None, "p2p_probe": p2p,
-                  "global_launches_per_step": len(glob) // len(timed), "avg_ms": round(d, 3)}
+    buckets = controlled_buckets(timed, res["unit_ms"], m) if args.workload == "controlled" and fusion == "none" \
+        else {}
+    nvlink = nvlink_summary(by_kind, world, p2p, len(timed))
+
+    # ------------------------ secondary objects: BASELINE configs 3 / 4 / 5 shapes, same slice
+    secondary = {}
+    if not args.no_secondary and args.n is None:
+        plan = [("controlled", "controlled", "none"), ("random_passes", "random", "passes"),
+                ("qft_passes", "qft", "passes"), ("qft_tolerance", "qft", "tolerance")]
+        for name, wl, fz in plan:
+            if wl == args.workload and fz == fusion:
+                continue
+            sc = step_circuits(sv, wl, n, args.warmup + args.steps, seed=1)
+            for c in sc[: args.warmup]:
+                for _, _, _, fn, _ in make_units(sv, c, m, fz, args.l_c, state, fabric):
+                    fn()
+            barrier()
+            r2 = timer.run(sc[args.warmup:], state, m, fabric, fz, args.l_c)
+            applied += [(c, fcfg_of(fz)) for c in sc]
+            rf, bk = roofline(r2, m, peaks, peak_kind)
+            ms = r2["elapsed_ms"]
+            obj = {"workload": WORKLOADS[wl].format(n=n, n1=n - 1),
+                   "fusion": fz if fz == "none" else f"{fz} (l_c={args.l_c})",
+                   "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
+                   "value": round(sum(effective_bytes(c, n) for c in sc[args.warmup:]) / (ms * 1e-3) / 1e9, 3),
+                   "unit": "GB/s", "gates_per_step": len(sc[-1]),
+                   "gates_per_s": round(sum(len(c) for c in sc[args.warmup:]) / (ms * 1e-3), 3),
+                   "hbm_passes_per_step": round(sum(len(u) for u in r2["units"]) / len(r2["units"]), 2),
+                   "roofline": rf, "gpu_launches": r2["launches"], "clocks": r2["clocks"]}
+            if wl == "controlled" and fz == "none":
+                obj["buckets"] = controlled_buckets(sc[args.warmup:], r2["unit_ms"], m)
+            nv2 = nvlink_summary(bk, world, p2p, args.steps)
+            if nv2:
+                obj["nvlink"] = nv2
+            secondary[name] = obj
+
+    # ------------------------------ N > 1: every exchange data plane on the same box
+    planes = None
+    if args.planes and world > 1 and fabric is not None:
+        planes = time_planes(sv, torch, dist, state, fabric, n, m, timer, args, p2p)
 
     # ------------------------------ self-check: inverse circuits restore the input
     self_check = None
     if initial is not None:
-        for c in reversed(circs):
-            sv.run_circuit(state, c.inverse(), fabric, fusion=fcfg)
+        tol_gates = 0
+        for c, fc in reversed(applied):
+            sv.run_circuit(state, c.inverse(), fabric, fusion=fc)
+            if fc is not None and not fc.exact:
+                tol_gates += 2 * len(c)
         from paper_1601_07195_b200.core import max_abs_diff
 
         err = max_abs_diff(state.amps, initial)
         if world > 1:
             err = reduce_scalar(err, dist.ReduceOp.MAX)
-        ng = 2 * sum(len(c) for c in circs)
+        ng = 2 * sum(len(c) for c, _ in applied)
         self_check = {"max_abs_err": err, "bound": 1e-12 * ng ** 0.5, "gates": ng,
                       "ok": err <= 1e-12 * ng ** 0.5,
-                      "what": "every warm-up and timed step undone by its inverse circuit, vs the saved input"}
+                      "what": "every warm-up and timed step (main and secondary) undone by its inverse circuit, "
+                              "vs the saved input"}
+        if tol_gates:
+            self_check["tolerance_mode_gates"] = tol_gates
         del initial
 
     # ---------------------------------------------- end to end (host buffers)
@@ -508,13 +714,13 @@ def main():
     cpu = None
     import psutil
 
+    fcfg = fcfg_of(fusion)
     local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
     host_fits = (16 << m) * local_world <= 0.6 * psutil.virtual_memory().total
     if not args.no_e2e and not host_fits:  # decided alike on every rank: no collective diverges
         e2e = {"value": None, "unit": "GB/s", "skipped": f"one pinned {16 << m}-byte slice per rank x "
                f"{local_world} ranks exceeds 60% of this node's {psutil.virtual_memory().total} bytes of RAM"}
     if not args.no_e2e and host_fits:
-        # pinned host buffers for every rank on this node must fit comfortably in RAM
         free_dev = torch.cuda.mem_get_info(dev)[0]
         # run_pipelined needs two or three device slots next to the state (three: upload i+1 runs
         # while download i-1 drains); otherwise the state itself is loaded and stored in turn
@@ -567,8 +773,8 @@ def main():
                        "remap": bool(args.remap and fabric is not None),
                        "l2": "no flush: slice >> 126 MB L2" if m >= 26 else "slice fits L2 (parity-size run)",
                        "seed": {"state": 0, "circuit": 1}},
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "self_check": self_check,
-            "clocks": clocks.summary(),
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": res["launches"],
+            "self_check": self_check, "clocks": res["clocks"],
         }
         if buckets:
             line["controlled_buckets"] = buckets
@@ -576,6 +782,10 @@ def main():
             line["per_target_gbps"] = per_target
         if nvlink:
             line["nvlink"] = nvlink
+        if planes:
+            line["planes"] = planes
+        if secondary:
+            line["secondary"] = secondary
         s = json.dumps(line)
         print(s, flush=True)
         if args.out:
@@ -585,5 +795,56 @@ def main():
         dist.destroy_process_group()
 
 
+def nvlink_summary(by_kind, world, p2p, steps):
+    glob = [r for k, rs in by_kind.items() if k in GLOBAL_KINDS for r in rs]
+    if world <= 1 or not glob:
+        return None
+    d = float(np.mean([r[1] for r in glob]))
+    ach = sum(r[0] for r in glob) / (sum(r[1] for r in glob) * 1e-3) / 1e9  # link bytes per direction / time
+    return {"achieved_gbs_per_direction": round(ach, 1),
+            "peak_nominal": 900.0, "peak_measured_p2p": p2p["gbs_per_direction"] if p2p else None,
+            "frac_nominal": round(ach / 900.0, 4),
+            "frac_measured": round(ach / p2p["gbs_per_direction"], 4) if p2p else None, "p2p_probe": p2p,
+            "global_launches_per_step": len(glob) // max(1, steps), "avg_ms": round(d, 3)}
+
+
+def time_planes(sv, torch, dist, state, fabric, n, m, timer, args, p2p):
+    """One global-qubit gate (target n-1) through each exchange data plane, same box, same slice:
+    the fused IPC kernel (product), copy-engine chunks, NCCL send/recv chunks (baseline)."""
+    out = {}
+    rng = np.random.default_rng(99)
+    circs = [sv.Circuit(n, [sv.GateOp(sv.random_unitary(rng), n - 1)]) for _ in range(args.warmup + 3)]
+    orig = fabric.data_plane
+    for plane in ("ipc", "ce", "nccl"):
+        fabric.data_plane = plane
+        for c in circs[: args.warmup]:
+            sv.run_circuit(state, c, fabric)
+        r = timer.run(circs[args.warmup:], state, m, fabric, "none", args.l_c)
+        ms = r["elapsed_ms"] / 3
+        gbs = (1 << (m + 4)) / (ms * 1e-3) / 1e9
+        out[plane] = {"ms_per_gate": round(ms, 3), "gbs_per_direction": round(gbs, 1),
+                      "frac_nominal": round(gbs / 900.0, 4),
+                      "frac_measured": round(gbs / p2p["gbs_per_direction"], 4) if p2p else None}
+        for c in reversed(circs):  # restore the slice for the self-check
+            sv.run_circuit(state, c.inverse(), fabric)
+    fabric.data_plane = orig
+    return out
+
+
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
+    args = parse(argv)
+    world = job_size(args)
+    _, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return 0
+    cmd = launch_command(args, argv, free_port())
+    if cmd is not None:  # fan out: one rank per GPU, rank 0 prints the line
+        return subprocess.call(cmd, env={**os.environ, "PYTHONUNBUFFERED": "1"})
+    run_ours(args, world, rank, local)
+    return 0
+
+
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

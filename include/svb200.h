@@ -106,6 +106,19 @@ int sv_plan_gates(int m, const sv_gate *gates, int ngates, int tile, int32_t *gr
 /* Execute one planned group (kind SV_GROUP_*), e.g. to time groups one by one. */
 int sv_apply_group(void *amps, int m, int kind, const sv_gate *gates, int ngates, int tile, void *stream);
 
+/* Flags of the *_ex planner entry points. */
+#define SV_FLAG_TOLERANCE 1 /* FusionConfig(exact=False): stage groups run k_dstage, which collapses every
+                             * diagonal gate whose control is outside the pass's four slot bits into one
+                             * per-amplitude factor (values equal mix()'s within rounding, not bit for bit;
+                             * north_star's 1e-12 sqrt(G) bound); the cost model plans for it.  0: exact. */
+/* sv_apply_gates / sv_plan_gates / sv_apply_group with flags (SV_FLAG_*); flags = 0 is the exact
+ * entry point.  No reference counterpart: the tolerance mode extends fusion.py:71-135's plans. */
+int sv_apply_gates_ex(void *amps, int m, const sv_gate *gates, int ngates, int tile, int flags, void *stream);
+int sv_plan_gates_ex(int m, const sv_gate *gates, int ngates, int tile, int flags, int32_t *group_end,
+                     int32_t *group_kind, int max_groups);
+int sv_apply_group_ex(void *amps, int m, int kind, const sv_gate *gates, int ngates, int tile, int flags,
+                      void *stream);
+
 /* Staged variant of sv_exchange for the NCCL data plane (NvlinkFabric(data_plane=
  * "nccl"), the reference's chunked pipeline distributed.py:205-290 over NCCL
  * send/recv): `buf` holds the partner's elements j0 .. j0+count_j-1 of this rank's
@@ -115,6 +128,13 @@ int sv_apply_group(void *amps, int m, int kind, const sv_gate *gates, int ngates
  * to 2^(c_local+1). */
 int sv_exchange_chunk(void *mine, void *buf, int m, int own_is_zero, int c_local, const double *q, uint64_t j0,
                       uint64_t count_j, void *stream);
+
+/* The reference's _pair_kernel on two contiguous chunk vectors (distributed.py:187-202): element i
+ * of `mine` pairs with element i of `theirs`; own_is_zero decides the operand order (this rank
+ * holds a0: keep mix(mine, theirs, q11, q12), return mix(mine, theirs, q21, q22); else the
+ * roles swap).  Both are updated in place (theirs = the returned values).  The staged data
+ * planes use it on packed chunks (case 5: the bit-c = 1 elements, distributed.py:341-422). */
+int sv_pair_update(void *mine, void *theirs, uint64_t count, int own_is_zero, const double *q, void *stream);
 
 /* A stage of gates that all target the same global qubit, applied in ONE
  * exchange (sv_exchange generalised to a gate list): each pair crosses NVLink

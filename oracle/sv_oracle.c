@@ -238,6 +238,40 @@ void or_fill_phase(double *amps_d, int m, int threads) {
   }
 }
 
+/* The seeded state of the GPU arm (sv_init_random: Philox4x32-10 with the global
+ * index as counter, Box-Muller), unnormalised, for the CPU reference arm's input.
+ * libm's log/sincos may differ from CUDA's in the last ulp: same distribution and
+ * seed, not a parity vector. */
+static void philox4x32(uint32_t c[4], uint32_t k0, uint32_t k1) {
+  for (int r = 0; r < 10; ++r) {
+    const uint64_t p0 = (uint64_t)0xD2511F53u * c[0], p1 = (uint64_t)0xCD9E8D57u * c[2];
+    const uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0, hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+    const uint32_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
+    c[0] = n0;
+    c[1] = lo1;
+    c[2] = n2;
+    c[3] = lo0;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+}
+
+void or_fill_philox(double *amps_d, int m, uint64_t gbase, uint64_t seed, int threads) {
+  c128 *amps = (c128 *)amps_d;
+  int64_t n = (int64_t)1 << m;
+#pragma omp parallel for schedule(static) num_threads(clamp_threads(threads))
+  for (int64_t i = 0; i < n; ++i) {
+    const uint64_t g = gbase + (uint64_t)i;
+    uint32_t c[4] = {(uint32_t)g, (uint32_t)(g >> 32), 0x51u, 0x7u};
+    philox4x32(c, (uint32_t)seed, (uint32_t)(seed >> 32));
+    const uint64_t b1 = ((uint64_t)c[0] << 32) | c[1], b2 = ((uint64_t)c[2] << 32) | c[3];
+    const double u1 = ((double)(b1 >> 11) + 1.0) * 0x1.0p-53, u2 = (double)(b2 >> 11) * 0x1.0p-53;
+    const double rad = sqrt(-2.0 * log(u1));
+    amps[i].re = rad * cos(6.283185307179586 * u2);
+    amps[i].im = rad * sin(6.283185307179586 * u2);
+  }
+}
+
 int or_max_threads(void) {
 #ifdef _OPENMP
   return omp_get_max_threads();

@@ -23,6 +23,7 @@ SV_STAGE_MAX_GATES = 64
 SV_MSTAGE_MAX_GATES, SV_MSTAGE_MAX_TARGETS = 128, 4
 SV_TILE_GATHER = 8
 SV_GROUP_GATES, SV_GROUP_TILE, SV_GROUP_STAGE = 0, 1, 2
+SV_FLAG_TOLERANCE = 1
 ABI_VERSION = 1
 
 EXPORTS = (
@@ -30,7 +31,8 @@ EXPORTS = (
     "sv_apply_fused", "sv_apply_gates", "sv_plan_gates", "sv_apply_group", "sv_exchange", "sv_exchange_chunk",
     "sv_exchange_stage", "sv_norm_sq", "sv_init_random", "sv_scale", "sv_init_basis",
     "sv_copy", "sv_ipc_handle", "sv_ipc_open", "sv_ipc_close", "sv_diag_global", "sv_diag_fix",
-    "sv_swap_global", "sv_max_abs_diff",
+    "sv_swap_global", "sv_max_abs_diff", "sv_apply_gates_ex", "sv_plan_gates_ex", "sv_apply_group_ex",
+    "sv_pair_update",
 )
 
 
@@ -71,8 +73,13 @@ def load() -> ctypes.CDLL:
         "sv_plan_gates": ([i, ctypes.POINTER(SvGate), i, i, ctypes.POINTER(ctypes.c_int32),
                            ctypes.POINTER(ctypes.c_int32), i], i),
         "sv_apply_group": ([vp, i, i, ctypes.POINTER(SvGate), i, i, vp], i),
+        "sv_apply_gates_ex": ([vp, i, ctypes.POINTER(SvGate), i, i, i, vp], i),
+        "sv_plan_gates_ex": ([i, ctypes.POINTER(SvGate), i, i, i, ctypes.POINTER(ctypes.c_int32),
+                              ctypes.POINTER(ctypes.c_int32), i], i),
+        "sv_apply_group_ex": ([vp, i, i, ctypes.POINTER(SvGate), i, i, i, vp], i),
         "sv_exchange": ([vp, vp, i, i, i, dp, vp], i),
         "sv_exchange_chunk": ([vp, vp, i, i, i, dp, u64, u64, vp], i),
+        "sv_pair_update": ([vp, vp, u64, i, dp, vp], i),
         "sv_exchange_stage": ([vp, vp, i, i, ctypes.POINTER(SvGate), i, vp], i),
         "sv_norm_sq": ([vp, i, i, vp, vp], i),
         "sv_init_random": ([vp, i, u64, u64, vp], i),

@@ -22,6 +22,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 
 #include "svb200.h"
 
@@ -1159,6 +1160,149 @@ __global__ void __launch_bounds__(MS_BLK, SV_MS_MINB * 256 / MS_BLK) k_mstage(do
   for (int j = 0; j < MS_N; ++j) a[base | ms_off(j, b)] = r[j];
 }
 
+// ------------------------------------- tolerance-mode stage passes (FusionConfig exact=False)
+//
+// The same thread layout as k_mstage (16 amplitudes spanning four slot bits,
+// every other index bit fixed per thread), but the gate list is compiled on the
+// host into a program that no longer reproduces mix()'s rounding sequence,
+// only its value (north_star: fused gates checked under max-abs <= 1e-12 sqrt(G)):
+//   fold   a diagonal gate on slot s whose control is not a slot (or absent):
+//          for a thread it means "multiply every amplitude with slot bit s = 1
+//          by d1 (= 0: by d0)" when the thread's own control bit is set.  The
+//          consecutive folds of one slot (a transform stage's R(k, c) for every
+//          c outside the pass) form a fold group whose product is a function of
+//          the thread's index bits only; k_dtable tabulates it per index byte
+//          (256 products per byte, built once per launch), so the group costs a
+//          thread one table load and one complex multiply per index byte.
+//   GATE   any other gate (general / real / Hadamard-like updates, diagonal
+//          gates controlled by another slot): in registers, as in k_mstage.
+//   FLUSH  multiply slot s's amplitudes by their fold group's product; emitted
+//          before the next non-diagonal gate whose target is s (a factor that
+//          depends only on bit s and the fixed bits commutes with every gate
+//          that does not target s) and at the end of the pass.
+// No zero tests, no replay.
+
+constexpr int DS_MAX = 256, DS_QMAX = 1280, DS_MAXG = 32;
+enum { DS_GATE = 0, DS_FLUSH = 2 };
+
+struct DsParams {
+  int32_t nops, nbytes;   // nbytes: index bytes a fold table covers (ceil(m / 8))
+  int32_t bits[MS_K];
+  const double2 *tab;     // k_dtable output: per group [T1: nbytes x 256][T0: nbytes x 256]
+  uint64_t hdr[DS_MAX];   // type 0-1 | slot 2-3 | cmode 4-5 (2: control on a non-slot bit) |
+                          // flags 6 (FLUSH: apply T0 too) | cbit 8-13 | code / group 16-23 | q offset 32-63
+  double q[DS_QMAX];
+};
+
+struct DtFold {
+  int8_t group, c;  // c: control slice bit, -1 uncontrolled
+  int16_t pad;
+  int32_t pad2;
+  double d[4];      // d0 re, im, d1 re, im
+};
+
+struct DtParams {
+  int32_t nfold, nbytes;
+  double2 *tab;
+  DtFold f[MS_MAX];
+};
+
+// One block per (group, index byte, table kind); thread v = the byte's value.
+__global__ void __launch_bounds__(256) k_dtable(const __grid_constant__ DtParams P) {
+  const int g = blockIdx.x / (2 * P.nbytes), k = (blockIdx.x / 2) % P.nbytes, one = (blockIdx.x & 1) == 0;
+  const int v = threadIdx.x;
+  double2 prod = make_double2(1.0, 0.0);
+  for (int i = 0; i < P.nfold; ++i) {
+    const DtFold &f = P.f[i];
+    if (f.group != g) continue;
+    const bool act = f.c < 0 ? k == 0 : ((f.c >> 3) == k && ((v >> (f.c & 7)) & 1));
+    if (act) prod = cmul(one ? f.d[2] : f.d[0], one ? f.d[3] : f.d[1], prod);
+  }
+  P.tab[((size_t)(g * 2 + (one ? 0 : 1)) * P.nbytes + k) * 256 + v] = prod;
+}
+
+__device__ __forceinline__ double2 cmul2(double2 f, double2 a) { return cmul(f.x, f.y, a); }
+
+__device__ __forceinline__ double2 ds_factor(const double2 *__restrict__ t, int nbytes, uint64_t base) {
+  double2 f = t[base & 255u];
+  for (int k = 1; k < nbytes; ++k) f = cmul2(t[k * 256 + ((base >> (8 * k)) & 255u)], f);
+  return f;
+}
+
+template <int S>
+__device__ __forceinline__ void ds_flush(double2 (&r)[MS_N], double2 f1, double2 f0, bool do0) {
+#pragma unroll
+  for (int j = 0; j < MS_N; ++j) {
+    if ((j >> S) & 1)
+      r[j] = cmul2(f1, r[j]);
+    else if (do0)
+      r[j] = cmul2(f0, r[j]);
+  }
+}
+
+__device__ __forceinline__ void ds_gate(int code, double2 (&r)[MS_N], const double *q) {
+  switch (code) {
+#define DS_CASE(K_, S_, C_)                       \
+  case ((K_) * MS_K + (S_)) * (MS_K + 1) + (C_): \
+    ms_apply<S_, C_, K_>(r, q);                   \
+    break;
+#if SV_MS_K == 3
+#define DS_CASES_S(K_, S_) DS_CASE(K_, S_, 0) DS_CASE(K_, S_, 1) DS_CASE(K_, S_, 2) DS_CASE(K_, S_, 3)
+#define DS_CASES(K_) DS_CASES_S(K_, 0) DS_CASES_S(K_, 1) DS_CASES_S(K_, 2)
+#else
+#define DS_CASES_S(K_, S_) \
+  DS_CASE(K_, S_, 0) DS_CASE(K_, S_, 1) DS_CASE(K_, S_, 2) DS_CASE(K_, S_, 3) DS_CASE(K_, S_, 4)
+#define DS_CASES(K_) DS_CASES_S(K_, 0) DS_CASES_S(K_, 1) DS_CASES_S(K_, 2) DS_CASES_S(K_, 3)
+#endif
+    DS_CASES(KIND_GENERAL) DS_CASES(KIND_DIAG) DS_CASES(KIND_PHASE) DS_CASES(KIND_REAL) DS_CASES(KIND_HSHARE)
+#undef DS_CASES
+#undef DS_CASES_S
+#undef DS_CASE
+    default: break;
+  }
+}
+
+#ifndef SV_DS_MINB
+#define SV_DS_MINB 2  // 256-thread CTAs per SM (measured QFT(30) tolerance passes: 2 -> 7.0 ms, 3 -> 7.7, 4 -> 11.0)
+#endif
+
+__global__ void __launch_bounds__(256, SV_DS_MINB) k_dstage(double2 *__restrict__ a, uint64_t ngroups,
+                                                           const __grid_constant__ DsParams P) {
+  const uint64_t p = (uint64_t)blockIdx.x * 256 + threadIdx.x;
+  if (p >= ngroups) return;
+  uint64_t b[MS_K], base = p;
+#pragma unroll
+  for (int s = 0; s < MS_K; ++s) {
+    b[s] = 1ull << P.bits[s];
+    base = insert_zero(base, P.bits[s]);
+  }
+  double2 r[MS_N];
+#pragma unroll
+  for (int j = 0; j < MS_N; ++j) r[j] = a[base | ms_off(j, b)];
+  const int nb = P.nbytes;
+  for (int i = 0; i < P.nops; ++i) {
+    const uint64_t h = P.hdr[i];
+    const int s = (int)((h >> 2) & 3u);
+    if ((h & 3u) == DS_FLUSH) {
+      const double2 *t = P.tab + (size_t)((h >> 16) & 0xffu) * 2 * nb * 256;
+      const double2 f1 = ds_factor(t, nb, base);
+      const bool do0 = (h >> 6) & 1u;
+      const double2 f0 = do0 ? ds_factor(t + nb * 256, nb, base) : make_double2(1.0, 0.0);
+      switch (s) {
+        case 0: ds_flush<0>(r, f1, f0, do0); break;
+        case 1: ds_flush<1>(r, f1, f0, do0); break;
+        case 2: ds_flush<2>(r, f1, f0, do0); break;
+        default: ds_flush<MS_K - 1>(r, f1, f0, do0); break;
+      }
+      continue;
+    }
+    if (((h >> 4) & 3u) == 2u && !((base >> ((h >> 8) & 63u)) & 1ull)) continue;  // control clear here
+    ds_gate((int)((h >> 16) & 0xffu), r, P.q + (h >> 32));
+  }
+#pragma unroll
+  for (int j = 0; j < MS_N; ++j) a[base | ms_off(j, b)] = r[j];
+}
+
 // ------------------------------------------------ diagonal gates on a global qubit
 //
 // a diagonal gate (q12 = q21 = 0 exactly) on a global target
@@ -1827,6 +1971,131 @@ int run_mstage(double2 *a, int m, const sv_gate *gates, int n, cudaStream_t st) 
   return after_launch("k_mstage");
 }
 
+// Per-device ring of fold-table buffers for k_dstage (the library's only cached device state,
+// besides nothing else: allocated once per device, never freed).  A launch takes the next
+// slot, so up to DT_SLOTS launches may be in flight on concurrent streams.
+constexpr int DT_SLOTS = 64;
+constexpr size_t DT_SLOT_BYTES = (size_t)DS_MAXG * 2 * 8 * 256 * sizeof(double2);  // 32 groups, 8 bytes of index
+
+double2 *dtable_slot() {
+  static std::mutex mu;
+  static double2 *ring[64] = {};
+  static std::atomic<unsigned> next[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (!ring[dev]) {
+      void *p = nullptr;
+      if (cudaMalloc(&p, DT_SLOTS * DT_SLOT_BYTES) != cudaSuccess) return nullptr;
+      ring[dev] = (double2 *)p;
+    }
+  }
+  const unsigned k = next[dev].fetch_add(1u) % DT_SLOTS;
+  return ring[dev] + k * (DT_SLOT_BYTES / sizeof(double2));
+}
+
+// Tolerance-mode stage launch (k_dtable + k_dstage): compile gates[0..n) (targets in <= MS_K
+// bits) into GATE / FLUSH ops and fold groups.
+int run_dstage(double2 *a, int m, const sv_gate *gates, int n, cudaStream_t st) {
+  static thread_local DsParams P;
+  static thread_local DtParams T;
+  if (n < 1 || n > MS_MAX) return fail(SV_EINVAL, "tolerance stage group: %d gates not in [1, %d]", n, MS_MAX);
+  if (m < MS_K) return fail(SV_EINVAL, "tolerance stage group: m=%d below %d", m, MS_K);
+  int bits[MS_K], nb = 0;
+  for (int k = 0; k < n; ++k) {
+    const int t = gates[k].target;
+    bool in = false;
+    for (int s = 0; s < nb; ++s) in |= bits[s] == t;
+    if (in) continue;
+    if (nb == MS_K) return fail(SV_EINVAL, "tolerance stage group: more than %d distinct targets", MS_K);
+    bits[nb++] = t;
+  }
+  // pad with high bits that are no gate's control (a slot control would turn a fold into a
+  // register update), then with any free bit
+  bool ctl[64] = {};
+  for (int k = 0; k < n; ++k)
+    if (gates[k].control >= 0) ctl[gates[k].control] = true;
+  for (int pass = 0; pass < 2; ++pass)
+    for (int b = m - 1; b >= 0 && nb < MS_K; --b) {
+      bool in = false;
+      for (int s = 0; s < nb; ++s) in |= bits[s] == b;
+      if (!in && (pass == 1 || !ctl[b])) bits[nb++] = b;
+    }
+  std::sort(bits, bits + MS_K);
+  auto slot = [&](int b) {
+    for (int s = 0; s < MS_K; ++s)
+      if (bits[s] == b) return s;
+    return MS_K;
+  };
+  const int nbytes = (m + 7) / 8;
+  int nops = 0, nq = 0, ngroups = 0;
+  int open_group[MS_K];
+  bool has0[DS_MAXG] = {};
+  for (int s = 0; s < MS_K; ++s) open_group[s] = -1;
+  T.nfold = 0;
+  auto emit = [&](uint64_t lo, const double *q, int nd) {
+    P.hdr[nops++] = lo | ((uint64_t)nq << 32);
+    if (nd) memcpy(P.q + nq, q, sizeof(double) * nd);
+    nq += nd;
+  };
+  auto flush = [&](int s) {
+    const int g = open_group[s];
+    emit((uint64_t)DS_FLUSH | ((uint64_t)s << 2) | ((uint64_t)(has0[g] ? 1 : 0) << 6) | ((uint64_t)g << 16),
+         nullptr, 0);
+    open_group[s] = -1;
+  };
+  for (int k = 0; k < n; ++k) {
+    const sv_gate &g = gates[k];
+    const int s = slot(g.target), c = g.control, cs = c >= 0 ? slot(c) : MS_K;
+    const int kind = gate_kind(g.q);
+    const bool diag = kind == KIND_DIAG || kind == KIND_PHASE;
+    if (diag && cs == MS_K) {
+      if (open_group[s] < 0) {
+        if (ngroups == DS_MAXG) return fail(SV_EINVAL, "tolerance stage group: more than %d fold groups", DS_MAXG);
+        open_group[s] = ngroups++;
+      }
+      DtFold &f = T.f[T.nfold++];
+      f.group = (int8_t)open_group[s];
+      f.c = (int8_t)c;
+      f.pad = 0;
+      f.pad2 = 0;
+      f.d[0] = g.q[0];
+      f.d[1] = g.q[1];
+      f.d[2] = g.q[6];
+      f.d[3] = g.q[7];
+      has0[open_group[s]] |= !(g.q[0] == 1.0 && g.q[1] == 0.0);
+      continue;
+    }
+    if (!diag && open_group[s] >= 0) flush(s);
+    const int code = (kind * MS_K + s) * (MS_K + 1) + cs;
+    const uint64_t cm = (c >= 0 && cs == MS_K) ? (2ull << 4) | ((uint64_t)(c & 63) << 8) : 0ull;
+    emit((uint64_t)DS_GATE | ((uint64_t)s << 2) | cm | ((uint64_t)code << 16), g.q, 8);
+  }
+  for (int s = 0; s < MS_K; ++s)
+    if (open_group[s] >= 0) flush(s);
+  P.nops = nops;
+  P.nbytes = nbytes;
+  for (int s = 0; s < MS_K; ++s) P.bits[s] = bits[s];
+  P.tab = nullptr;
+  if (ngroups) {
+    double2 *tab = dtable_slot();
+    if (!tab) return fail(SV_ECUDA, "tolerance stage group: fold-table buffer allocation failed");
+    T.nbytes = nbytes;
+    T.tab = tab;
+    P.tab = tab;
+    k_dtable<<<ngroups * nbytes * 2, 256, 0, st>>>(T);
+    const int rc = after_launch("k_dtable");
+    if (rc != SV_OK) return rc;
+  }
+  const uint64_t ng = 1ull << (m - MS_K);
+  k_dstage<<<grid_for(ng, 256), 256, 0, st>>>(a, ng, P);
+  return after_launch("k_dstage");
+}
+// ops <= gates + flushes, and every flush follows a fold and precedes a gate (or ends the pass)
+static_assert(DS_MAX >= 3 * MS_MAX / 2 + MS_K && DS_QMAX >= 8 * MS_MAX, "k_dstage program capacity");
+static_assert(DT_SLOT_BYTES >= (size_t)DS_MAXG * 2 * ((62 + 7) / 8) * 256 * sizeof(double2), "fold-table slot");
+
 // Native pass planner: the launch group starting at gates[i], returned as its end.
 // Candidate 1, a register-tiled run: targets below L = T-G, or one of up to G
 // (TG_BITS) higher slice bits taken in order of appearance (the tile then
@@ -1842,12 +2111,15 @@ int run_mstage(double2 *a, int m, const sv_gate *gates, int n, cudaStream_t st) 
 #define SV_PLAN_LOOKAHEAD 1  // measured: QFT(30) 74.2 -> 72.2 ms (one tail tile instead of stage + tile), controlled steps -2 %
 #endif
 
-double stage_cost(const sv_gate &g) {
+double stage_cost(const sv_gate &g, bool tol) {
   static const double c[KIND_COUNT] = {0.9, 0.35, 0.18, 0.55, 0.35};
-  return c[gate_kind(g.q)] * (g.control >= 0 ? 0.5 : 1.0);
+  const int k = gate_kind(g.q);
+  // tolerance mode: a diagonal gate folds into a per-thread factor (one multiply per 16 amplitudes)
+  if (tol && (k == KIND_DIAG || k == KIND_PHASE)) return 0.02;
+  return c[k] * (g.control >= 0 ? 0.5 : 1.0);
 }
 
-int next_group(int m, const sv_gate *gates, int n, int i, int T, int *kind) {
+int next_group(int m, const sv_gate *gates, int n, int i, int T, int *kind, bool tol = false) {
   const int L = T - TG_BITS;
   auto tile_cost = [&](int k) {
     static const double c[KIND_COUNT] = {1.15, 0.45, 0.45, 0.75, 0.55};
@@ -1879,7 +2151,7 @@ int next_group(int m, const sv_gate *gates, int n, int i, int T, int *kind) {
         if (ns == MS_K) break;
         S[ns++] = tt;
       }
-      cs += stage_cost(gates[jb]);
+      cs += stage_cost(gates[jb], tol);
     }
   }
   const int A = ja - i, B = jb - i;
@@ -1908,10 +2180,10 @@ int next_group(int m, const sv_gate *gates, int n, int i, int T, int *kind) {
   return ja;
 }
 
-int exec_group(double2 *a, int m, int T, int kind, const sv_gate *gates, int n, cudaStream_t st) {
+int exec_group(double2 *a, int m, int T, int kind, const sv_gate *gates, int n, cudaStream_t st, bool tol = false) {
   if (kind == SV_GROUP_STAGE) {
     if (n == 1) return launch_gate(a, m, gates[0], st);
-    return run_mstage(a, m, gates, n, st);
+    return tol ? run_dstage(a, m, gates, n, st) : run_mstage(a, m, gates, n, st);
   }
   if (kind == SV_GROUP_TILE && T >= 9 && n > 1) {
     const int L = T - TG_BITS;
@@ -2031,29 +2303,36 @@ int sv_apply_fused(void *amps, int m, int l, const sv_gate *gates, int ngates, v
   return launch_fused((double2 *)amps, m, T, P, (cudaStream_t)stream);
 }
 
-int sv_apply_gates(void *amps, int m, const sv_gate *gates, int ngates, int tile, void *stream) {
+int sv_apply_gates_ex(void *amps, int m, const sv_gate *gates, int ngates, int tile, int flags, void *stream) {
   if (bad_ptr(amps) || (!gates && ngates)) return fail(SV_EINVAL, "sv_apply_gates: null or misaligned pointer");
   if (m < 1 || m > 62) return fail(SV_EINVAL, "sv_apply_gates: m=%d out of range", m);
   if (ngates < 0) return fail(SV_EINVAL, "sv_apply_gates: negative gate count");
+  if (flags & ~SV_FLAG_TOLERANCE) return fail(SV_EINVAL, "sv_apply_gates: unknown flags %#x", flags);
   int rc = check_gates("sv_apply_gates", m, gates, ngates, m);
   if (rc != SV_OK) return rc;
   const int tmax = m < SV_FUSED_MAX_TILE ? m : SV_FUSED_MAX_TILE;
   const int T = tile > 0 ? tile : tmax;
   if (tile != 0 && (tile < 9 || tile > tmax)) return fail(SV_EINVAL, "sv_apply_gates: tile %d not in [9, %d]", tile, tmax);
+  const bool tol = flags & SV_FLAG_TOLERANCE;
   int i = 0;
   while (i < ngates && rc == SV_OK) {
     int kind;
-    const int j = next_group(m, gates, ngates, i, T, &kind);
-    rc = exec_group((double2 *)amps, m, T, kind, gates + i, j - i, (cudaStream_t)stream);
+    const int j = next_group(m, gates, ngates, i, T, &kind, tol);
+    rc = exec_group((double2 *)amps, m, T, kind, gates + i, j - i, (cudaStream_t)stream, tol);
     i = j;
   }
   return rc;
 }
 
-int sv_plan_gates(int m, const sv_gate *gates, int ngates, int tile, int32_t *group_end, int32_t *group_kind,
-                  int max_groups) {
+int sv_apply_gates(void *amps, int m, const sv_gate *gates, int ngates, int tile, void *stream) {
+  return sv_apply_gates_ex(amps, m, gates, ngates, tile, 0, stream);
+}
+
+int sv_plan_gates_ex(int m, const sv_gate *gates, int ngates, int tile, int flags, int32_t *group_end,
+                     int32_t *group_kind, int max_groups) {
   if ((!gates && ngates) || !group_end || !group_kind) return fail(SV_EINVAL, "sv_plan_gates: null pointer");
   if (m < 1 || m > 62 || ngates < 0) return fail(SV_EINVAL, "sv_plan_gates: m=%d / ngates=%d invalid", m, ngates);
+  if (flags & ~SV_FLAG_TOLERANCE) return fail(SV_EINVAL, "sv_plan_gates: unknown flags %#x", flags);
   int rc = check_gates("sv_plan_gates", m, gates, ngates, m);
   if (rc != SV_OK) return rc;
   const int tmax = m < SV_FUSED_MAX_TILE ? m : SV_FUSED_MAX_TILE;
@@ -2063,7 +2342,7 @@ int sv_plan_gates(int m, const sv_gate *gates, int ngates, int tile, int32_t *gr
   while (i < ngates) {
     if (ng == max_groups) return fail(SV_EINVAL, "sv_plan_gates: more than %d groups", max_groups);
     int kind;
-    i = next_group(m, gates, ngates, i, T, &kind);
+    i = next_group(m, gates, ngates, i, T, &kind, flags & SV_FLAG_TOLERANCE);
     group_end[ng] = i;
     group_kind[ng] = kind;
     ++ng;
@@ -2071,15 +2350,27 @@ int sv_plan_gates(int m, const sv_gate *gates, int ngates, int tile, int32_t *gr
   return ng;
 }
 
-int sv_apply_group(void *amps, int m, int kind, const sv_gate *gates, int ngates, int tile, void *stream) {
+int sv_plan_gates(int m, const sv_gate *gates, int ngates, int tile, int32_t *group_end, int32_t *group_kind,
+                  int max_groups) {
+  return sv_plan_gates_ex(m, gates, ngates, tile, 0, group_end, group_kind, max_groups);
+}
+
+int sv_apply_group_ex(void *amps, int m, int kind, const sv_gate *gates, int ngates, int tile, int flags,
+                      void *stream) {
   if (bad_ptr(amps) || !gates) return fail(SV_EINVAL, "sv_apply_group: null or misaligned pointer");
   if (m < 1 || m > 62 || ngates < 1) return fail(SV_EINVAL, "sv_apply_group: m=%d / ngates=%d invalid", m, ngates);
+  if (flags & ~SV_FLAG_TOLERANCE) return fail(SV_EINVAL, "sv_apply_group: unknown flags %#x", flags);
   int rc = check_gates("sv_apply_group", m, gates, ngates, m);
   if (rc != SV_OK) return rc;
   const int tmax = m < SV_FUSED_MAX_TILE ? m : SV_FUSED_MAX_TILE;
   if (tile != 0 && (tile < 9 || tile > tmax)) return fail(SV_EINVAL, "sv_apply_group: tile %d not in [9, %d]", tile, tmax);
   if (kind < SV_GROUP_GATES || kind > SV_GROUP_STAGE) return fail(SV_EINVAL, "sv_apply_group: kind %d", kind);
-  return exec_group((double2 *)amps, m, tile > 0 ? tile : tmax, kind, gates, ngates, (cudaStream_t)stream);
+  return exec_group((double2 *)amps, m, tile > 0 ? tile : tmax, kind, gates, ngates, (cudaStream_t)stream,
+                    flags & SV_FLAG_TOLERANCE);
+}
+
+int sv_apply_group(void *amps, int m, int kind, const sv_gate *gates, int ngates, int tile, void *stream) {
+  return sv_apply_group_ex(amps, m, kind, gates, ngates, tile, 0, stream);
 }
 
 int sv_exchange_stage(void *mine, void *theirs, int m, int own_is_zero, const sv_gate *gates, int ngates,
@@ -2194,6 +2485,15 @@ int sv_exchange_chunk(void *mine, void *buf, int m, int own_is_zero, int c_local
   k_exchange<<<grid_for(count, BLK * UNROLL), BLK, 0, (cudaStream_t)stream>>>(
       (double2 *)mine, theirs, count, j0, c_local, own_is_zero ? 1 : 0, load_q(q));
   return after_launch("sv_exchange_chunk");
+}
+
+int sv_pair_update(void *mine, void *theirs, uint64_t count, int own_is_zero, const double *q, void *stream) {
+  if (bad_ptr(mine) || bad_ptr(theirs) || !q) return fail(SV_EINVAL, "sv_pair_update: null or misaligned pointer");
+  if (mine == theirs) return fail(SV_EINVAL, "sv_pair_update: the two chunks alias");
+  if (count == 0) return SV_OK;
+  k_exchange<<<grid_for(count, BLK * UNROLL), BLK, 0, (cudaStream_t)stream>>>(
+      (double2 *)mine, (double2 *)theirs, count, 0, -1, own_is_zero ? 1 : 0, load_q(q));
+  return after_launch("sv_pair_update");
 }
 
 int sv_norm_sq(const void *amps, int m, int qubit, double *scratch, void *stream) {

@@ -28,6 +28,8 @@ from __future__ import annotations
 import ctypes
 import enum
 import threading
+import time
+import warnings
 from dataclasses import dataclass
 
 import numpy as np
@@ -108,11 +110,12 @@ def make_exchange_plan(layout, k: int, *, chunk_amps: int | None = None, chunk_b
 
 
 class ScratchPool:
-    """API-compatible scratch accounting (distributed.py:161-181).
+    """Recycled chunk buffers with high-water accounting (distributed.py:161-181).
 
-    The fused exchange stages nothing, so the pool is never drawn from by the
-    gate path and ``high_water_bytes`` stays 0; take/give keep working for
-    callers that use it directly.
+    The fused IPC exchange stages nothing and never draws from it; the staged
+    data planes (NCCL send/recv and copy-engine chunks) take their two chunk
+    buffers here, so ``high_water_bytes`` is 2 * chunk * 16 B for them, the
+    reference's bound.
     """
 
     def __init__(self):
@@ -231,6 +234,54 @@ class CudaExecutor:
     def view(self, state: LocalState, j0: int, num_amps: int) -> torch.Tensor:
         return state.amps[j0:j0 + num_amps]
 
+    def pair_update(self, mine: torch.Tensor, buf: torch.Tensor, own_is_zero: bool, q: GateMatrix) -> None:
+        """_pair_kernel on two contiguous chunk vectors (sv_pair_update)."""
+        with torch.cuda.device(mine.device):
+            _lib.check(_lib.load().sv_pair_update(mine.data_ptr(), buf.data_ptr(), mine.numel(), int(own_is_zero),
+                                                  _as_gate(q).qbuf(), stream_handle()))
+
+    def tensor(self, state: LocalState) -> torch.Tensor:
+        return state.amps
+
+    def buffer_device(self, state: LocalState) -> torch.device:
+        return state.amps.device
+
+    def ce_exchange(self, state: LocalState, theirs: int, own_is_zero: bool, segments, q: GateMatrix,
+                    bufs) -> None:
+        """Copy-engine data plane: for each (j0, count, c_local) segment of this rank's computing
+        half, cudaMemcpyAsync the partner's elements into a local chunk buffer (copy-in stream),
+        update with the exchange kernel (current stream), push the partner's results back
+        (copy-out stream).  Two buffers: chunk i+1 streams in while chunk i computes and
+        chunk i-1 drains."""
+        ptr, m = device_view(state.amps)
+        dev = state.amps.device
+        lib = _lib.load()
+        qb = _as_gate(q).qbuf()
+        with torch.cuda.device(dev):
+            main = torch.cuda.current_stream(dev)
+            s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+            s_in.wait_stream(main)
+            freed = [None] * len(bufs)  # event: buffer b's previous push-back is done
+            for i, (j0, cnt, cl) in enumerate(segments):
+                b = i % len(bufs)
+                buf = bufs[b]
+                if freed[b] is not None:
+                    s_in.wait_event(freed[b])
+                _lib.check(lib.sv_copy(buf.data_ptr(), theirs + j0 * AMP_BYTES, cnt * AMP_BYTES, s_in.cuda_stream))
+                got = torch.cuda.Event()
+                got.record(s_in)
+                main.wait_event(got)
+                _lib.check(lib.sv_exchange_chunk(ptr, buf.data_ptr(), m, int(own_is_zero), int(cl), qb, j0, cnt,
+                                                 main.cuda_stream))
+                done = torch.cuda.Event()
+                done.record(main)
+                s_out.wait_event(done)
+                _lib.check(lib.sv_copy(theirs + j0 * AMP_BYTES, buf.data_ptr(), cnt * AMP_BYTES, s_out.cuda_stream))
+                freed[b] = torch.cuda.Event()
+                freed[b].record(s_out)
+            main.wait_stream(s_out)
+            main.wait_stream(s_in)
+
     def exchange_stage(self, state: LocalState, theirs: int, own_is_zero: bool, ops) -> None:
         from .kernels import gate_array
 
@@ -239,17 +290,19 @@ class CudaExecutor:
             _lib.check(_lib.load().sv_exchange_stage(ptr, theirs, m, int(own_is_zero), gate_array(ops), len(ops),
                                                      stream_handle()))
 
-    def local_gates(self, state: LocalState, ops, tile: int = 0, group: int | None = None) -> None:
-        """sv_apply_gates (planner inside), or sv_apply_group for one pre-planned group."""
+    def local_gates(self, state: LocalState, ops, tile: int = 0, group: int | None = None,
+                    exact: bool = True) -> None:
+        """sv_apply_gates_ex (planner inside), or sv_apply_group_ex for one pre-planned group;
+        exact=False is the tolerance mode (SV_FLAG_TOLERANCE)."""
         from .kernels import apply_gates, gate_array
 
         if group is None:
-            apply_gates(state.amps, ops, tile)
+            apply_gates(state.amps, ops, tile, exact=exact)
             return
         ptr, m = device_view(state.amps)
         with torch.cuda.device(state.amps.device):
-            _lib.check(_lib.load().sv_apply_group(ptr, m, int(group), gate_array(ops), len(ops), int(tile),
-                                                  stream_handle()))
+            _lib.check(_lib.load().sv_apply_group_ex(ptr, m, int(group), gate_array(ops), len(ops), int(tile),
+                                                     0 if exact else _lib.SV_FLAG_TOLERANCE, stream_handle()))
 
     def synchronize(self, state: LocalState) -> None:
         torch.cuda.current_stream(state.amps.device).synchronize()
@@ -318,16 +371,46 @@ class CudaExecutor:
 _CUDA = CudaExecutor()
 
 
+FP_MASK = (1 << 62) - 1
+
+
+def fingerprint(*fields) -> int:
+    """Deterministic 62-bit protocol word of one fenced step (same on every rank that agrees
+    on the step; the reference's wire phase words, distributed.py:46-47)."""
+    h = 0x345678
+    for f in fields:
+        h = ((h ^ (int(f) & 0xFFFFFFFFFFFF)) * 1000003 + 0x9E3779B1) & FP_MASK
+    return h
+
+
 class NvlinkFabric:
     """Exchange fabric over one torch.distributed group, one rank per GPU.
 
     Stands in for the reference's ``transport`` argument everywhere
     (apply_op, run_circuit, global_norm_sq, gather_full_state).  Counters
     follow CountingTransport: payload bytes sent / received over the link.
+
+    Data planes: "ipc" (default, the product) -- the fused exchange kernel on
+    the partner's CUDA-IPC-mapped slice; "ce" -- copy-engine chunks
+    (cudaMemcpyAsync of peer chunks into a local double buffer, the exchange
+    kernel, an async push back); "nccl" -- the reference's staged pipeline
+    (distributed.py:205-290) over NCCL send/recv, double-buffered, at most two
+    chunks in flight (the baseline, and the fallback when peer mapping is
+    refused).
+
+    Fences fail loudly (the reference's TransportError on a timeout or a phase
+    desync, transport.py:56-79): every fence all-reduces (max) this rank's
+    protocol fingerprint and its negation, so ranks that disagree on the step
+    -- different gate, chunking or plan -- see max != min and raise
+    ``TransportError``; a fence that does not complete within ``timeout_s``
+    raises too.  Host fences (gloo) check at once; stream fences (NCCL) are
+    checked without a host sync every ``check_every`` fences and at the end of
+    each ``run_circuit`` (``check``).
     """
 
     def __init__(self, group=None, *, fence: str | None = None, executor=None, data_plane: str = "ipc",
-                 chunk_amps: int = 1 << 26, diagonal_local: bool = False):
+                 chunk_amps: int = 1 << 26, diagonal_local: bool = False, timeout_s: float = 300.0,
+                 check_every: int = 64):
         import torch.distributed as dist
 
         if not dist.is_initialized():
@@ -340,22 +423,21 @@ class NvlinkFabric:
         self.fence_mode = fence or ("stream" if backend == "nccl" else "host")
         if self.fence_mode not in ("stream", "host"):
             raise ValueError("fence must be 'stream' or 'host'")
-        if data_plane not in ("ipc", "nccl"):
-            raise ValueError("data_plane must be 'ipc' or 'nccl'")
-        # "ipc": fused kernel on the partner's mapped slice (the product).  "nccl": the
-        # reference's staged pipeline over send/recv (baseline, and the fallback when
-        # peer mapping is refused); switched collectively in ensure_registered.
+        if data_plane not in ("ipc", "ce", "nccl"):
+            raise ValueError("data_plane must be 'ipc', 'ce' or 'nccl'")
         self.data_plane = data_plane
         self.chunk_amps = chunk_amps
-        self._scratch: torch.Tensor | None = None
+        self.scratch = ScratchPool()
         self.executor = executor or _CUDA
         self.sent_bytes = 0
         self.received_bytes = 0
         self.fences = 0
+        self.timeout_s = float(timeout_s)
+        self.check_every = int(check_every)
+        self._pending: list = []
         self._tag = CONTROL_TAG
         self._lock = threading.Lock()
         self._peers: dict[tuple, tuple[list, list]] = {}
-        self._flag: torch.Tensor | None = None
         # SURVEY.md 8(f)1, off by default (it departs from the reference's per-gate traffic
         # contract, test_acceptance.py:61-71): diagonal gates on global qubits run without an
         # exchange.  Must be the same on every rank.
@@ -365,7 +447,12 @@ class NvlinkFabric:
     @property
     def diag_mode(self) -> bool:
         """Diagonal global gates take the no-exchange path (needs peer mappings)."""
-        return self.diagonal_local and self.data_plane == "ipc"
+        return self.diagonal_local and self.data_plane in ("ipc", "ce")
+
+    @property
+    def mapped(self) -> bool:
+        """The data plane works on CUDA-IPC-mapped peer slices."""
+        return self.data_plane in ("ipc", "ce")
 
     # --- Transport-compatible surface
     def fresh_tag(self) -> int:
@@ -387,7 +474,10 @@ class NvlinkFabric:
 
     def exchange_objects(self, obj) -> list:
         out = [None] * self.num_ranks
-        self._dist.all_gather_object(out, obj, group=self.group)
+        try:
+            self._dist.all_gather_object(out, obj, group=self.group)
+        except RuntimeError as exc:  # gloo/NCCL timeout or a dead peer
+            raise TransportError(f"object exchange failed: {exc}") from exc
         return out
 
     def reduce_sum(self, partial: float) -> float:
@@ -397,75 +487,142 @@ class NvlinkFabric:
             total += v
         return total
 
-    def barrier(self, state: LocalState | None = None) -> None:
+    # --- fences
+    def fence(self, state: LocalState | None = None, fp: int = 0) -> None:
+        """Collective fence that also checks every rank is at the same protocol step."""
+        import torch.distributed as dist
+
         self.fences += 1
+        fp &= FP_MASK
         if self.fence_mode == "stream":
             dev = self.executor.flag_device(state)
-            if self._flag is None or self._flag.device != dev:
-                self._flag = torch.zeros(1, dtype=torch.int32, device=dev)
-            self._dist.all_reduce(self._flag, group=self.group)
-        else:
-            if state is not None:
-                self.executor.synchronize(state)
-            self._dist.barrier(group=self.group)
+            t = torch.empty(2, dtype=torch.int64, device=dev)
+            t[0].fill_(fp)
+            t[1].fill_(-fp)
+            self._dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+            self._pending.append((fp, t, self.fences))
+            if len(self._pending) >= self.check_every:
+                self.check(state)
+            return
+        if state is not None:
+            self.executor.synchronize(state)
+        t = torch.tensor([fp, -fp], dtype=torch.int64)
+        try:
+            self._dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+        except RuntimeError as exc:
+            raise TransportError(f"fence {self.fences} failed or timed out: {exc}") from exc
+        self._verify(fp, t, self.fences)
+
+    def barrier(self, state: LocalState | None = None) -> None:
+        """A fence with the neutral fingerprint (register/gather/teardown points)."""
+        self.fence(state, 0)
+
+    def _verify(self, fp: int, t, where: int) -> None:
+        hi, lo = int(t[0]), -int(t[1])
+        if hi != fp or lo != fp:
+            raise TransportError(
+                f"protocol desync at fence {where}: this rank is at step {fp:#x}, the ranks span "
+                f"[{lo:#x}, {hi:#x}] (different gate, plan or chunking on some rank)")
+
+    def check(self, state: LocalState | None = None) -> None:
+        """Wait (at most timeout_s) for the stream fences issued so far and verify them."""
+        if not self._pending:
+            return
+        pend, self._pending = self._pending, []
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(pend[-1][1].device))
+        deadline = time.monotonic() + self.timeout_s
+        while not ev.query():
+            if time.monotonic() > deadline:
+                raise TransportError(f"fence {pend[-1][2]} did not complete within {self.timeout_s:g} s "
+                                     "(a rank diverged from the gate sequence or died)")
+            time.sleep(2e-4)
+        vals = torch.stack([t for _, t, _ in pend]).cpu()
+        for (fp, _, where), v in zip(pend, vals):
+            self._verify(fp, v, where)
 
     # --- peer mappings
     def ensure_registered(self, state: LocalState) -> None:
         """Collective: map every rank's slice into this process (once per slice).
 
-        If any rank cannot export or map a slice, every rank drops its mappings and
-        switches to the NCCL data plane together (the decision is all-gathered, so
-        the ranks never disagree on the protocol)."""
-        if self.data_plane == "nccl":
+        Every rank takes part in every collective whatever happens locally: the
+        export blobs are all-gathered (None from a rank that failed), then every
+        rank's success.  If any rank cannot export or map a slice, every rank
+        drops its mappings and switches to the NCCL data plane together.  The
+        sign maps of diagonal_local follow the same two-step pattern; if they
+        fail anywhere, diagonal gates go back to exchanges on every rank."""
+        if not self.mapped:
             return
         key = self.executor.key(state)
         if key in self._peers:
             return
         err = None
+        mine = None
         try:
             mine = self.executor.share(state)
         except Exception as exc:  # noqa: BLE001 -- reported below, collectively
-            mine, err = None, exc
+            err = exc
         blobs = self.exchange_objects(mine)
         ptrs = [None] * self.num_ranks
-        if err is None and all(b is not None for b in blobs):
+        if err is None and any(b is None for b in blobs):
+            err = TransportError("a peer could not export its slice")
+        if err is None:
             for r, blob in enumerate(blobs):
-                if r != self.rank:
-                    try:
-                        ptrs[r] = self.executor.open(state, blob)
-                    except Exception as exc:  # noqa: BLE001
-                        err = exc
-                        break
-        diag = None
-        if err is None and self.diagonal_local:
-            try:
-                diag = self._register_signs(state, ptrs)
-            except Exception as exc:  # noqa: BLE001
-                err = exc
+                if r == self.rank:
+                    continue
+                try:
+                    ptrs[r] = self.executor.open(state, blob)
+                except Exception as exc:  # noqa: BLE001
+                    err = exc
+                    break
         ok = self.exchange_objects(err is None)
-        if all(ok):
-            self._peers[key] = (ptrs, blobs)
-            if diag is not None:
-                self._diag[key] = diag
+        if not all(ok):
+            self._close_all(ptrs, blobs)
+            warnings.warn(f"peer mapping refused on some rank ({err!r} here); exchanges fall back to NCCL "
+                          "send/recv")
+            self.data_plane = "nccl"
             return
-        if diag is not None:
-            for r, p in enumerate(diag[2]):
-                if p is not None:
-                    self.executor.close(p, diag[3][r])
+        self._peers[key] = (ptrs, blobs)
+        if self.diagonal_local:
+            self._register_signs(state, key)
+
+    def _close_all(self, ptrs, blobs) -> None:
         for r, p in enumerate(ptrs):
             if p is not None:
-                self.executor.close(p, blobs[r])
-        import warnings
+                try:
+                    self.executor.close(p, blobs[r])
+                except Exception:  # noqa: BLE001 -- best effort while falling back
+                    pass
 
-        warnings.warn(f"peer mapping refused on some rank ({err!r} here); exchanges fall back to NCCL send/recv")
-        self.data_plane = "nccl"
-
-    def _register_signs(self, state: LocalState, ptrs) -> tuple:
+    def _register_signs(self, state: LocalState, key) -> None:
         """Sign map + flag of this slice, and every peer's sign map mapped here (collective)."""
-        signs, flag = self.executor.diag_alloc(state)
-        blobs = self.exchange_objects(self.executor.share_buffer(state, signs))
-        peers = [None if r == self.rank else self.executor.open(state, b) for r, b in enumerate(blobs)]
-        return signs, flag, peers, blobs
+        err, blob, signs, flag = None, None, None, None
+        try:
+            signs, flag = self.executor.diag_alloc(state)
+            blob = self.executor.share_buffer(state, signs)
+        except Exception as exc:  # noqa: BLE001
+            err = exc
+        blobs = self.exchange_objects(blob)
+        peers = [None] * self.num_ranks
+        if err is None and any(b is None for b in blobs):
+            err = TransportError("a peer could not export its sign map")
+        if err is None:
+            for r, b in enumerate(blobs):
+                if r == self.rank:
+                    continue
+                try:
+                    peers[r] = self.executor.open(state, b)
+                except Exception as exc:  # noqa: BLE001
+                    err = exc
+                    break
+        ok = self.exchange_objects(err is None)
+        if all(ok):
+            self._diag[key] = (signs, flag, peers, blobs)
+            return
+        self._close_all(peers, blobs)
+        warnings.warn(f"sign-map registration failed on some rank ({err!r} here); diagonal global gates "
+                      "exchange as usual")
+        self.diagonal_local = False
 
     def diag_buffers(self, state: LocalState):
         try:
@@ -480,48 +637,123 @@ class NvlinkFabric:
         except (KeyError, IndexError) as exc:
             raise TransportError("peer sign map not registered") from exc
 
-    def nccl_exchange(self, state: LocalState, action: GateAction, q: GateMatrix) -> int:
-        """The reference's half exchange over send/recv (distributed.py:205-311), staged in
-        chunks through one scratch buffer.  Returns payload bytes sent (== received).
+    # --- staged data planes
+    def _global_peer(self, rank: int) -> int:
+        return rank if self.group is None else self._dist.get_global_rank(self.group, rank)
 
-        Stage s covers half s; its computing rank (zero side for s = 0) receives the
-        partner's chunk, updates both with sv_exchange_chunk and sends the partner's
-        updated elements back; the passive rank sends its chunk and receives it
-        updated, straight into its slice.  Case 5 moves whole chunks (the kernel
-        updates only local-bit-c elements)."""
-        dist = self._dist
+    def staged_exchange(self, state: LocalState, action: GateAction, q: GateMatrix, chunk: int | None = None,
+                        scratch: ScratchPool | None = None) -> int:
+        """One gate's exchange on the staged planes ("nccl", "ce").  Returns the payload bytes
+        this rank sent (== received)."""
+        if self.data_plane == "ce":
+            return ce_exchange(self, state, action, q, chunk, scratch)
+        return self.nccl_exchange(state, action, q, chunk, scratch)
+
+    def nccl_exchange(self, state: LocalState, action: GateAction, q: GateMatrix, chunk: int | None = None,
+                      scratch: ScratchPool | None = None) -> int:
+        """The reference's half exchange over send/recv (distributed.py:205-422): per half,
+        the computing rank receives the partner's chunks into two scratch buffers, updates
+        both with the pair kernel and returns the partner's elements; the passive rank streams
+        its chunks out (at most two in flight) and receives them updated.  Case 5 packs the
+        bit-c = 1 elements of each half first (``_packed_control_slice``), so only they cross."""
         ex = self.executor
         m = state.layout.m
         half = 1 << (m - 1)
-        chunk = min(self.chunk_amps, half)
-        peer = action.partner if self.group is None else dist.get_global_rank(self.group, action.partner)
+        whole = ex.tensor(state)
+        peer = self._global_peer(action.partner)
+        pool = scratch if scratch is not None else self.scratch
+        chunk = chunk or self.chunk_amps
+        c = action.c_local
         moved = 0
         for stage in (0, 1):
-            c_local = action.c_local
-            if c_local == m - 1:  # the half-selecting bit: only the second half holds control-set pairs
+            region = whole[stage * half:(stage + 1) * half]
+            sel = None
+            if c == m - 1:  # the half-selecting bit: only the second half holds control-set pairs
                 if stage == 0:
                     continue
-                c_local = -1
-            computing = action.own_is_zero == (stage == 0)
-            if computing and (self._scratch is None or self._scratch.numel() < chunk):
-                self._scratch = ex.scratch(state, chunk)
-            for j0 in range(stage * half, (stage + 1) * half, chunk):
-                if computing:
-                    buf = self._scratch[:chunk]
-                    self._recv(buf, peer)
-                    ex.exchange_chunk(state, buf, action.own_is_zero, c_local, q, j0, chunk)
-                    self._send(buf, peer)
+                vec = region
+            elif c >= 0:
+                sel = region.view(-1, 2, 1 << c)[:, 1, :]
+                if sel.is_contiguous():  # c = m - 2: one run, already packed
+                    vec, sel = sel.reshape(-1), None
                 else:
-                    view = ex.view(state, j0, chunk)
-                    self._send(view, peer)
-                    self._recv(view, peer)
-                moved += chunk * AMP_BYTES
+                    vec = sel.contiguous().view(-1)
+            else:
+                vec = region
+            computing = action.own_is_zero == (stage == 0)
+            self._pipeline(state, vec, computing, action.own_is_zero, q, chunk, pool, peer)
+            if sel is not None:
+                sel.copy_(vec.view(sel.shape))
+            moved += vec.numel() * AMP_BYTES
         return moved
+
+    def _pipeline(self, state, vec, computing: bool, own_is_zero: bool, q, chunk: int, pool, peer: int) -> None:
+        """chunked_exchange_pipeline (distributed.py:205-290) over torch.distributed p2p.
+        Both sides issue their operations in one global order (computing: R0 R1 S0 R2 S1 R3 ...,
+        passive: S0 S1 R0 S2 R1 S3 ...), so blocking (gloo) and stream-ordered (NCCL)
+        transports pair them identically and never deadlock; NCCL overlaps chunk i+1's
+        transfer with chunk i's update."""
+        total = vec.numel()
+        if total == 0:
+            return
+        chunk = min(chunk, total)
+        steps = -(-total // chunk)
+        span = [(i * chunk, min(total, (i + 1) * chunk)) for i in range(steps)]
+        works = []
+        if not computing:
+            for i in range(min(2, steps)):
+                works.append(self._isend(vec[span[i][0]:span[i][1]], peer))
+            for i in range(steps):
+                lo, hi = span[i]
+                works.append(self._irecv(vec[lo:hi], peer))
+                if i + 2 < steps:
+                    works.append(self._isend(vec[span[i + 2][0]:span[i + 2][1]], peer))
+            self._wait_all(works)
+            return
+        nbuf = min(2, steps)
+        dev = self.executor.buffer_device(state)
+        bufs = [pool.take(chunk, device=dev) for _ in range(nbuf)]
+        try:
+            recvs = {}
+            for i in range(nbuf):
+                lo, hi = span[i]
+                recvs[i] = self._irecv(bufs[i % nbuf][:hi - lo], peer)
+            for i in range(steps):
+                lo, hi = span[i]
+                buf = bufs[i % nbuf][:hi - lo]
+                self._wait_all([recvs.pop(i)])
+                self.executor.pair_update(vec[lo:hi], buf, own_is_zero, q)
+                works.append(self._isend(buf, peer))
+                if i + 2 < steps:
+                    lo2, hi2 = span[i + 2]
+                    recvs[i + 2] = self._irecv(bufs[i % nbuf][:hi2 - lo2], peer)
+            self._wait_all(works)
+        finally:
+            for b in bufs:
+                pool.give(b)
+
+    def _isend(self, t: torch.Tensor, peer: int):
+        if self.fence_mode == "host":  # gloo: blocking, host memory
+            self._send(t, peer)
+            return None
+        return self._dist.isend(t, dst=peer, group=self.group)
+
+    def _irecv(self, t: torch.Tensor, peer: int):
+        if self.fence_mode == "host":
+            self._recv(t, peer)
+            return None
+        return self._dist.irecv(t, src=peer, group=self.group)
+
+    def _wait_all(self, works: list) -> None:
+        for w in works:
+            if w is not None:
+                w.wait()  # NCCL: the current stream waits, the host does not
+        works.clear()
 
     def _send(self, t: torch.Tensor, peer: int) -> None:
         if t.is_cuda and self.fence_mode == "host":  # gloo moves host memory only
             t = t.cpu()
-        self._dist.send(t, dst=peer, group=self.group)
+        self._dist.send(t.contiguous(), dst=peer, group=self.group)
 
     def _recv(self, t: torch.Tensor, peer: int) -> None:
         if t.is_cuda and self.fence_mode == "host":
@@ -546,32 +778,52 @@ class NvlinkFabric:
         key = self.executor.key(state)
         entry = self._peers.pop(key, None)
         if entry:
-            for ptr, blob in zip(*entry):
-                if ptr is not None:
-                    self.executor.close(ptr, blob)
+            self._close_all(*entry)
         diag = self._diag.pop(key, None)
         if diag:
-            for ptr, blob in zip(diag[2], diag[3]):
-                if ptr is not None:
-                    self.executor.close(ptr, blob)
+            self._close_all(diag[2], diag[3])
 
     def close(self) -> None:
         for key in list(self._diag):
             _, _, ptrs, blobs = self._diag.pop(key)
-            for ptr, blob in zip(ptrs, blobs):
-                if ptr is not None:
-                    try:
-                        self.executor.close(ptr, blob)
-                    except Exception:
-                        pass
+            self._close_all(ptrs, blobs)
         for key in list(self._peers):
             ptrs, blobs = self._peers.pop(key)
-            for ptr, blob in zip(ptrs, blobs):
-                if ptr is not None:
-                    try:
-                        self.executor.close(ptr, blob)
-                    except Exception:
-                        pass
+            self._close_all(ptrs, blobs)
+
+
+def ce_exchange(fabric, state: LocalState, action: GateAction, q: GateMatrix, chunk: int | None = None,
+            scratch: ScratchPool | None = None) -> int:
+    """Copy-engine data plane: this rank computes its half of the pair space (zero side the
+    first, one side the second, as the fused kernel) through two local chunk buffers;
+    chunks whose elements all have control bit c clear are skipped."""
+    m = state.layout.m
+    half = 1 << (m - 1)
+    lo = 0 if action.own_is_zero else half
+    c = action.c_local
+    if c == m - 1:
+        if action.own_is_zero:
+            return 0
+        c = -1
+    chunk = min(chunk or fabric.chunk_amps, half)
+    segs = []
+    for j0 in range(lo, lo + half, chunk):
+        if c >= 0 and (2 << c) > chunk:  # the chunk lies on one side of bit c
+            if (j0 >> c) & 1:
+                segs.append((j0, chunk, -1))
+        else:
+            segs.append((j0, chunk, c))
+    pool = scratch if scratch is not None else fabric.scratch
+    dev = fabric.executor.buffer_device(state)
+    bufs = [pool.take(chunk, device=dev) for _ in range(min(2, len(segs)))]
+    try:
+        if segs:
+            fabric.executor.ce_exchange(state, fabric.peer_pointer(state, action.partner), action.own_is_zero, segs,
+                                      q, bufs)
+    finally:
+        for b in bufs:
+            pool.give(b)
+    return sum(cnt for _, cnt, _ in segs) * AMP_BYTES
 
 
 class InprocFabric:
@@ -581,20 +833,34 @@ class InprocFabric:
     the caller runs each gate rank by rank on one stream (engine.run_circuit_inproc), so
     stream order is the fence.  Same exchange kernels, same counters as NvlinkFabric."""
 
-    data_plane = "ipc"
     diagonal_local = False
     diag_mode = False
+    mapped = True
 
-    def __init__(self, states, rank: int):
+    def __init__(self, states, rank: int, data_plane: str = "ipc", chunk_amps: int = 1 << 26):
+        if data_plane not in ("ipc", "ce"):
+            raise ValueError("in-process ranks run the 'ipc' (fused kernel) or 'ce' (copy-engine) plane")
         self.states, self.rank, self.num_ranks = states, rank, len(states)
+        self.data_plane = data_plane
+        self.chunk_amps = chunk_amps
+        self.scratch = ScratchPool()
         self.executor = _CUDA
         self.sent_bytes = self.received_bytes = 0
         self.fences = 0
         self._tag = CONTROL_TAG
 
     @classmethod
-    def group(cls, states) -> list["InprocFabric"]:
-        return [cls(states, r) for r in range(len(states))]
+    def group(cls, states, data_plane: str = "ipc", chunk_amps: int = 1 << 26) -> list["InprocFabric"]:
+        return [cls(states, r, data_plane, chunk_amps) for r in range(len(states))]
+
+    def staged_exchange(self, state, action, q, chunk=None, scratch=None) -> int:
+        return ce_exchange(self, state, action, q, chunk, scratch)
+
+    def fence(self, state=None, fp: int = 0) -> None:
+        self.fences += 1
+
+    def check(self, state=None) -> None:
+        pass
 
     def fresh_tag(self) -> int:
         self._tag += 1
@@ -629,9 +895,26 @@ class InprocFabric:
         pass
 
 
+def _fence(fabric, state, fp: int) -> None:
+    fence = getattr(fabric, "fence", None)
+    if fence is not None:
+        fence(state, fp)
+    else:
+        fabric.barrier(state)
+
+
+def step_fingerprint(tag: int, target: int, control: int | None, chunk: int | None = None, what: int = 0) -> int:
+    """Protocol word of one fenced gate: every participating and idle rank computes the same
+    value when they agree on the gate, its plan's chunking and the step kind."""
+    return fingerprint(tag, target, -1 if control is None else control, chunk or 0, what)
+
+
 def execute_action(state: LocalState, action: GateAction, q: GateMatrix, fabric: NvlinkFabric | None,
-                   executor=None) -> None:
-    """Run one rank's share of one gate; fences bracket every exchange-class gate on all ranks."""
+                   executor=None, *, tag: int | None = None, chunk: int | None = None,
+                   scratch: ScratchPool | None = None) -> None:
+    """Run one rank's share of one gate; fences bracket every exchange-class gate on all ranks.
+    A fence that finds the ranks at different steps, or times out, raises TransportError
+    and marks the slice corrupt (distributed.py:293-311, transport.py:56-79)."""
     ex = executor or (fabric.executor if fabric is not None else _CUDA)
     if action.kind == "single":
         ex.single(state, action.target, q)
@@ -641,28 +924,39 @@ def execute_action(state: LocalState, action: GateAction, q: GateMatrix, fabric:
         return
     if fabric is None:
         raise LayoutError(f"gate on qubit {action.target} needs a transport")
+    # rank-independent: participating, idle and diagonal-path ranks all fence with the same word
+    fp = step_fingerprint(getattr(fabric, "_tag", 0) if tag is None else tag, action.target, action.control, chunk)
     if action.kind == "diag":
-        _execute_diag(state, action, q, fabric, ex)
+        _execute_diag(state, action, q, fabric, ex, fp)
         return
     try:
         # Partner slices are read and written in place: every rank's prior
         # work must be complete before, and the exchange complete after.
-        fabric.barrier(state)
-        if action.kind == "exchange" and getattr(fabric, "data_plane", "ipc") == "nccl":
-            moved = fabric.nccl_exchange(state, action, q)
+        _fence(fabric, state, fp)
+        plane = getattr(fabric, "data_plane", "ipc")
+        if action.kind == "exchange" and plane in ("nccl", "ce"):
+            moved = fabric.staged_exchange(state, action, q, chunk, scratch)
             fabric.count(moved, moved)
         else:
             if action.kind == "exchange":
                 ex.exchange(state, fabric.peer_pointer(state, action.partner), action.own_is_zero, action.c_local,
                             q)
             fabric.count(action.sent, action.received)
-        fabric.barrier(state)
+        _fence(fabric, state, fp)
+    except TransportError:
+        state.corrupt = True
+        raise
+    except Exception as exc:  # a failed collective (timeout, dead peer) surfaces as the reference's error
+        state.corrupt = True
+        if isinstance(exc, (ValueError, LayoutError)):
+            raise
+        raise TransportError(f"exchange for qubit {action.target} failed: {exc}") from exc
     except BaseException:
         state.corrupt = True
         raise
 
 
-def _execute_diag(state, action, q, fabric, ex) -> None:
+def _execute_diag(state, action, q, fabric, ex, fp: int = 0) -> None:
     """Diagonal gate on a global qubit without an exchange (sv_diag_global / sv_diag_fix):
     own elements multiplied in place, then -- after a fence, so the partner's sign map of
     its original elements is complete -- zero components patched from that map.  The
@@ -671,10 +965,10 @@ def _execute_diag(state, action, q, fabric, ex) -> None:
     try:
         signs, flag = fabric.diag_buffers(state)
         ex.diag_global(state, action.own_is_zero, action.c_local, q, signs, flag)
-        fabric.barrier(state)
+        _fence(fabric, state, fp)
         ex.diag_fix(state, action.own_is_zero, action.c_local, q, fabric.peer_signs(state, action.partner), flag)
         fabric.count(0, 0)
-        fabric.barrier(state)
+        _fence(fabric, state, fp)
     except BaseException:
         state.corrupt = True
         raise
@@ -707,9 +1001,10 @@ def apply_single_distributed(state: LocalState, k: int, q: GateMatrix, transport
         raise LayoutError("distributed gate application needs at least 2 ranks")
     if not lay.m <= k < lay.n:
         raise LayoutError(f"qubit {k} is local (m={lay.m}); use the local kernel")
+    explicit = plan.chunk_amps if plan is not None else chunk_amps
     if plan is None:
         plan = make_exchange_plan(lay, k, chunk_amps=chunk_amps)
-    apply_global(state, k, None, q, transport, plan=plan)
+    apply_global(state, k, None, q, transport, plan=plan, chunk=explicit, scratch=scratch)
 
 
 def apply_controlled_distributed(state: LocalState, c: int, t: int, q: GateMatrix, transport: NvlinkFabric, *,
@@ -727,29 +1022,34 @@ def apply_controlled_distributed(state: LocalState, c: int, t: int, q: GateMatri
     if c < m and t < m:
         apply_controlled_raw(state.amps, c, t, q, policy)
         return
+    explicit = plan.chunk_amps if plan is not None else chunk_amps
     if t >= m and plan is None:
         plan = make_exchange_plan(lay, t, chunk_amps=chunk_amps)
-    apply_global(state, t, c, q, transport, plan=plan)
+    apply_global(state, t, c, q, transport, plan=plan, chunk=explicit, scratch=scratch)
 
 
 def apply_global(state, target: int, control: int | None, q, transport, *, plan: ExchangePlan | None = None,
-                 executor=None) -> None:
+                 executor=None, chunk: int | None = None, scratch: ScratchPool | None = None) -> None:
     """Shared tail of the distributed entry points: one gate touching a rank bit.
 
     Every rank calls it for every such gate (SPMD), so the collective pieces
-    -- fresh tag, slice registration, fences -- line up across ranks.
+    -- fresh tag, slice registration, fences -- line up across ranks.  ``chunk``
+    (the caller's explicit plan / chunk_amps) sets the staged planes' chunking
+    and enters the fence fingerprint, so ranks with different plans fail loudly
+    (the reference's test_mismatched_plans_fail_loudly, pkg/tests/test_distributed.py:218-235).
     """
     lay = state.layout
     _check_transport(transport, lay)
-    transport.fresh_tag()
+    tag = transport.fresh_tag()
     transport.ensure_registered(state)  # collective; may switch every rank to the NCCL data plane
     diag = getattr(transport, "diag_mode", False) and is_diagonal(q)
     action = plan_gate(lay, target, control, diag=diag)
     if plan is not None and action.kind == "exchange" and (
             plan.partner != action.partner
             or (plan.this_rank_computes is ComputesHalf.FIRST_HALF) != action.own_is_zero):
+        state.corrupt = True
         raise TransportError("exchange plan does not match this rank's pairing")
-    execute_action(state, action, _as_gate(q), transport, executor)
+    execute_action(state, action, _as_gate(q), transport, executor, tag=tag, chunk=chunk, scratch=scratch)
 
 
 def apply_op(state: LocalState, op, transport: NvlinkFabric | None = None, *, policy: ThreadPolicy = SERIAL,
@@ -787,9 +1087,9 @@ def gather_full_state(state: LocalState, transport: NvlinkFabric | None = None,
     if transport is None:
         raise LayoutError("gather requires a transport when p > 0")
     _check_transport(transport, lay)
-    transport.fresh_tag()
+    tag = transport.fresh_tag()
     transport.ensure_registered(state)
-    transport.barrier(state)
+    _fence(transport, state, fingerprint(tag, 0x6A7E))
     full = None
     nccl = getattr(transport, "data_plane", "ipc") == "nccl"
     if lay.rank == 0:
@@ -805,5 +1105,8 @@ def gather_full_state(state: LocalState, transport: NvlinkFabric | None = None,
         full = dev.cpu().numpy()
     elif nccl:
         transport._send(state.amps, 0)
-    transport.barrier(state)
+    _fence(transport, state, fingerprint(tag, 0x6A7E))
+    check = getattr(transport, "check", None)
+    if check is not None:
+        check(state)
     return full

@@ -31,15 +31,25 @@ class FusionConfig:
 
     ``passes=True`` (an extension, off by default so plans match the
     reference) replaces block runs by the native pass planner of passes.py:
-    l_c then sets the register tile (clamped to [9, 13])."""
+    l_c then sets the register tile (clamped to [9, 13]).
+
+    ``exact=False`` (with ``passes=True`` only; opt-in) trades bitwise parity for
+    fewer operations: consecutive gates on the same qubits multiply into one
+    2x2 matrix and stage passes collapse every diagonal gate controlled from
+    outside the pass into one per-amplitude factor (k_dstage).  Results then
+    match the reference within rounding -- north_star's max-abs <= 1e-12 sqrt(G)
+    bound for fused gates -- instead of bit for bit."""
 
     l_c: int
     enabled: bool = True
     passes: bool = False
+    exact: bool = True
 
     def __post_init__(self):
         if self.l_c < 1:
             raise ValueError("block exponent must be >= 1")
+        if not self.exact and not self.passes:
+            raise ValueError("exact=False needs passes=True (the tolerance mode is a pass-planner mode)")
 
 
 def default_block_exponent(llc_bytes: int, m: int) -> int:
@@ -69,6 +79,7 @@ class FusionPlan:
     l_c: int
     segments: list = field(default_factory=list)
     passes: bool = False
+    exact: bool = True
 
     def flatten(self) -> list[GateOp]:
         out: list[GateOp] = []
@@ -82,7 +93,7 @@ class FusionPlan:
 
 def plan_fusion(circuit: Circuit, config: FusionConfig) -> FusionPlan:
     """Greedy maximal runs in circuit order, no reordering (fusion.py:71-94)."""
-    plan = FusionPlan(config.l_c, passes=config.enabled and config.passes)
+    plan = FusionPlan(config.l_c, passes=config.enabled and config.passes, exact=config.exact or not config.enabled)
     if plan.passes:  # the pass planner needs m; execute_plan cuts the passes
         plan.segments = [PassThrough(op) for op in circuit]
         return plan
@@ -143,7 +154,7 @@ def execute_plan(state: LocalState, plan: FusionPlan, policy: ThreadPolicy = SER
         from .passes import execute_pass, plan_passes, tile_for
 
         tile = tile_for(plan.l_c, state.layout.m)
-        for p in plan_passes(plan.flatten(), state.layout.m, tile):
+        for p in plan_passes(plan.flatten(), state.layout.m, tile, exact=plan.exact):
             execute_pass(state, p, transport, tile=tile)
         return
     if plan.l_c > state.layout.m:

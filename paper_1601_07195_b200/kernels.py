@@ -203,11 +203,12 @@ def launch_fused(amps, ops: list, l: int) -> None:
             _lib.check(lib.sv_apply_fused(ptr, m, int(l), gate_array(part), len(part), stream_handle()))
 
 
-def apply_gates(amps, ops, tile: int = 0) -> None:
+def apply_gates(amps, ops, tile: int = 0, exact: bool = True) -> None:
     """Native pass planner (sv_apply_gates): local gates applied in order, grouped into
     register-tiled runs (targets < tile, controls anywhere) and multi-target stage passes
     (runs whose targets lie in at most four qubits).
-    Bit-identical to applying them one by one."""
+    Bit-identical to applying them one by one; exact=False: the tolerance mode
+    (SV_FLAG_TOLERANCE, equal within rounding)."""
     ptr, m = device_view(amps)
     ops = list(ops)
     if not ops:
@@ -216,7 +217,8 @@ def apply_gates(amps, ops, tile: int = 0) -> None:
         if op.max_qubit() >= m:
             raise LayoutError(f"gate on qubits {op.qubits()} is not local (m={m})")
     with torch.cuda.device(amps.device):
-        _lib.check(_lib.load().sv_apply_gates(ptr, m, gate_array(ops), len(ops), int(tile), stream_handle()))
+        _lib.check(_lib.load().sv_apply_gates_ex(ptr, m, gate_array(ops), len(ops), int(tile),
+                                                 0 if exact else _lib.SV_FLAG_TOLERANCE, stream_handle()))
 
 
 def apply_block(block_amps, gates: Iterable["GateOp"], policy: ThreadPolicy = SERIAL) -> None:

@@ -23,18 +23,29 @@ sees the same updates in the same order, and the structure-specialised
 updates (diagonal / phase / real / Hadamard-like gates) are exact -- they
 differ from mix() only in zero signs, and any zero in a pass's final values
 sends that group through an exact replay (svb200.cu "speculative pair updates").
+
+``exact=False`` (FusionConfig(passes=True, exact=False), the tolerance mode):
+before planning, a gate merges into the latest earlier gate that acts on
+exactly its qubits in the same roles when nothing in between touched them (the
+product of the two 2x2 matrices; ``merge_gates``), and stage passes run
+k_dstage, which folds every diagonal gate controlled from outside the pass
+into one per-amplitude factor.  Values agree with the reference within
+rounding (north_star: max-abs <= 1e-12 sqrt(G), fused gates included), not bit
+for bit.
 """
 
 from __future__ import annotations
 
 from dataclasses import dataclass
 
+import numpy as np
+
 from . import _lib
 from .circuits import GateOp
-from .distributed import _CUDA, GateAction, _check_transport, apply_global
+from .distributed import _CUDA, GateAction, _check_transport, _fence, apply_global, fingerprint
 from .perfmodel import BoundCase
-from .errors import LayoutError
-from .kernels import _as_gate
+from .errors import LayoutError, TransportError
+from .kernels import GateMatrix, _as_gate
 
 
 LOCAL_KINDS = ("local_tile", "local_stage", "local_gate")
@@ -45,13 +56,35 @@ class Pass:
     kind: str                # local_tile | local_stage | local_gate | global_stage | global_gate
     gates: tuple[GateOp, ...]
     target: int | None = None
+    exact: bool = True       # False: tolerance mode (stage passes through k_dstage)
 
     @property
     def local(self) -> bool:
         return self.kind in LOCAL_KINDS
 
 
-def plan_passes(gates, m: int, tile: int = 0) -> list[Pass]:
+def merge_gates(gates) -> list[GateOp]:
+    """Tolerance mode: a gate multiplies into the latest earlier gate with the same target and
+    control when no gate in between touched either qubit (those gates commute with it), so
+    e.g. repeated rotations of one qubit become one 2x2 matrix.  Pure host arithmetic."""
+    out: list[GateOp] = []
+    last: dict[int, int] = {}
+    for op in gates:
+        qs = op.qubits()
+        j = last.get(qs[0], -1)
+        if j >= 0 and all(last.get(q, -1) == j for q in qs):
+            prev = out[j]
+            if prev.target == op.target and prev.control == op.control:
+                mat = np.asarray(_as_gate(op.gate).mat) @ np.asarray(_as_gate(prev.gate).mat)
+                out[j] = GateOp(GateMatrix.unchecked(mat), op.target, op.control, prev.name)
+                continue
+        out.append(op)
+        for q in qs:
+            last[q] = len(out) - 1
+    return out
+
+
+def plan_passes(gates, m: int, tile: int = 0, exact: bool = True) -> list[Pass]:
     """Cut a gate sequence into HBM passes -- a pure function of the gates, m and the tile,
     so every rank derives the same list (the collective fences line up).
 
@@ -59,8 +92,9 @@ def plan_passes(gates, m: int, tile: int = 0) -> list[Pass]:
     ``local_tile`` pass, a multi-target ``local_stage`` pass, or a lone ``local_gate``.
     Global targets: a run sharing the target is one ``global_stage`` exchange.  This is the
     grouping ``sv_apply_gates`` applies natively, exposed so each pass can be
-    timed and recorded on its own."""
-    gates = list(gates)
+    timed and recorded on its own.  exact=False: the tolerance mode (``merge_gates``
+    first, stage passes planned and run for k_dstage)."""
+    gates = list(gates) if exact else merge_gates(gates)
     out: list[Pass] = []
     i, n = 0, len(gates)
     while i < n:
@@ -69,11 +103,11 @@ def plan_passes(gates, m: int, tile: int = 0) -> list[Pass]:
         if t >= m:
             while j < n and gates[j].target == t and j - i < _lib.SV_STAGE_MAX_GATES:
                 j += 1
-            out.append(Pass("global_stage" if j - i > 1 else "global_gate", tuple(gates[i:j]), t))
+            out.append(Pass("global_stage" if j - i > 1 else "global_gate", tuple(gates[i:j]), t, exact))
         else:
             while j < n and gates[j].target < m:
                 j += 1
-            out.extend(_plan_local(gates[i:j], m, tile))
+            out.extend(_plan_local(gates[i:j], m, tile, exact))
         i = j
     return out
 
@@ -83,7 +117,7 @@ _GROUP_KIND = {_lib.SV_GROUP_GATES: "local_gate", _lib.SV_GROUP_TILE: "local_til
 _KIND_GROUP = {v: k for k, v in _GROUP_KIND.items()}
 
 
-def _plan_local(ops, m: int, tile: int) -> list[Pass]:
+def _plan_local(ops, m: int, tile: int, exact: bool = True) -> list[Pass]:
     """Split a run of local-target gates into launch groups with the native planner
     (sv_plan_gates, the one sv_apply_gates executes).  Rank-bit controls only decide
     per rank whether a gate applies, so they are planned as uncontrolled."""
@@ -96,12 +130,13 @@ def _plan_local(ops, m: int, tile: int) -> list[Pass]:
         arr[k].q[:] = list(_as_gate(op.gate).qbuf())
     ends = (ctypes.c_int32 * len(ops))()
     kinds = (ctypes.c_int32 * len(ops))()
-    ng = _lib.load().sv_plan_gates(m, arr, len(ops), int(tile), ends, kinds, len(ops))
+    ng = _lib.load().sv_plan_gates_ex(m, arr, len(ops), int(tile), 0 if exact else _lib.SV_FLAG_TOLERANCE,
+                                      ends, kinds, len(ops))
     if ng < 0:
         _lib.check(ng)
     out, start = [], 0
     for g in range(ng):
-        out.append(Pass(_GROUP_KIND[kinds[g]], tuple(ops[start:ends[g]]), ops[start].target))
+        out.append(Pass(_GROUP_KIND[kinds[g]], tuple(ops[start:ends[g]]), ops[start].target, exact))
         start = ends[g]
     return out
 
@@ -125,7 +160,10 @@ def execute_pass(state, p: Pass, transport=None, *, tile: int = 0, executor=None
     if p.local:
         ops = _resolve_rank_controls(p.gates, lay)
         if ops:
-            ex.local_gates(state, ops, tile, group=_KIND_GROUP[p.kind])
+            if p.exact:
+                ex.local_gates(state, ops, tile, group=_KIND_GROUP[p.kind])
+            else:
+                ex.local_gates(state, ops, tile, group=_KIND_GROUP[p.kind], exact=False)
         return
     if transport is None:
         raise LayoutError(f"gate on qubit {p.target} >= m={lay.m} requires a transport")
@@ -134,25 +172,32 @@ def execute_pass(state, p: Pass, transport=None, *, tile: int = 0, executor=None
         apply_global(state, op.target, op.control, op.gate, transport, executor=executor)
         return
     _check_transport(transport, lay)
-    transport.fresh_tag()
+    tag = transport.fresh_tag()
     transport.ensure_registered(state)
     bit = p.target - lay.m
     partner = lay.rank ^ (1 << bit)
     zero = ((lay.rank >> bit) & 1) == 0
     ops = [GateOp(_as_gate(op.gate), op.target, op.control, op.name)
            for op in _resolve_rank_controls(p.gates, lay)]
+    fp = fingerprint(tag, p.target, len(p.gates), 0x57A6E)
     try:
-        transport.barrier(state)
-        if ops and getattr(transport, "data_plane", "ipc") == "nccl":
-            for op in ops:  # staged fallback: one send/recv exchange per gate of the stage
+        _fence(transport, state, fp)
+        if ops and getattr(transport, "data_plane", "ipc") in ("nccl", "ce"):
+            for op in ops:  # staged planes: one chunked exchange per gate of the stage
                 act = GateAction("exchange", BoundCase.SINGLE_REMOTE, op.target, op.control, partner=partner,
                                  own_is_zero=zero, c_local=-1 if op.control is None else op.control)
-                moved = transport.nccl_exchange(state, act, op.gate)
+                moved = transport.staged_exchange(state, act, op.gate)
                 transport.count(moved, moved)
         elif ops:
             ex.exchange_stage(state, transport.peer_pointer(state, partner), zero, ops)
             transport.count(1 << (lay.m + 4), 1 << (lay.m + 4))
-        transport.barrier(state)
+        _fence(transport, state, fp)
+    except TransportError:
+        state.corrupt = True
+        raise
+    except Exception as exc:
+        state.corrupt = True
+        raise TransportError(f"stage exchange for qubit {p.target} failed: {exc}") from exc
     except BaseException:
         state.corrupt = True
         raise

@@ -114,28 +114,74 @@ def plan_remapped(gates, n: int, m: int, restore: bool = True, qmap: QubitMap | 
 
 
 def swap_global(state, sw: Swap, transport, executor=None) -> None:
-    """One rank's side of a global<->local swap, between two partner fences."""
-    from .distributed import _check_transport
+    """One rank's side of a global<->local swap, between two partner fences.  Peer-mapped
+    planes run k_swap_global on the partner's slice; the NCCL plane sends the moving half
+    (bit l = 1 - b) and receives the partner's in its place, chunk by chunk."""
+    from .distributed import _check_transport, _fence, fingerprint
 
     lay = state.layout
     _check_transport(transport, lay)
     if not (lay.m <= sw.global_bit < lay.n and 0 <= sw.local_bit < lay.m):
         raise LayoutError(f"swap ({sw.global_bit}, {sw.local_bit}) is not global <-> local for m={lay.m}")
-    transport.fresh_tag()
+    tag = transport.fresh_tag()
     transport.ensure_registered(state)
-    if getattr(transport, "data_plane", "ipc") != "ipc":
-        raise TransportError("qubit remapping needs peer-mapped slices (data_plane='ipc')")
     ex = executor or transport.executor
     bit = sw.global_bit - lay.m
     partner = lay.rank ^ (1 << bit)
+    b = (lay.rank >> bit) & 1
+    fp = fingerprint(tag, sw.global_bit, sw.local_bit, 0x5A9)
     try:
-        transport.barrier(state)
-        ex.swap_global(state, transport.peer_pointer(state, partner), ((lay.rank >> bit) & 1) == 0, sw.local_bit)
+        _fence(transport, state, fp)
+        if getattr(transport, "mapped", True):
+            ex.swap_global(state, transport.peer_pointer(state, partner), b == 0, sw.local_bit)
+        else:
+            _swap_staged(transport, state, sw.local_bit, b, partner)
         transport.count(1 << (lay.m + 3), 1 << (lay.m + 3))
-        transport.barrier(state)
+        _fence(transport, state, fp)
+    except TransportError:
+        state.corrupt = True
+        raise
+    except Exception as exc:
+        state.corrupt = True
+        raise TransportError(f"swap of qubits ({sw.global_bit}, {sw.local_bit}) failed: {exc}") from exc
     except BaseException:
         state.corrupt = True
         raise
+
+
+def _swap_staged(fabric, state, l: int, b: int, partner: int) -> None:
+    """The swap over send/recv: own elements with bit l = 1 - b <-> the partner's with bit l = b,
+    in the same (row, column) order on both sides; pieces of at most chunk_amps elements."""
+    import torch.distributed as dist
+
+    whole = fabric.executor.tensor(state)
+    sel = whole.view(-1, 2, 1 << l)[:, 1 - b, :]
+    rows, width = sel.shape
+    chunk = max(1, fabric.chunk_amps)
+    if width >= chunk:
+        pieces = [sel[r, c0:c0 + chunk] for r in range(rows) for c0 in range(0, width, chunk)]
+    else:
+        per = max(1, chunk // width)
+        pieces = [sel[r0:r0 + per] for r0 in range(0, rows, per)]
+    peer = fabric._global_peer(partner)
+    dev = fabric.executor.buffer_device(state)
+    for piece in pieces:
+        out = piece.contiguous().view(-1)
+        inb = fabric.scratch.take(out.numel(), device=dev)
+        try:
+            if fabric.fence_mode == "stream":
+                for w in dist.batch_isend_irecv([dist.P2POp(dist.isend, out, peer, fabric.group),
+                                                 dist.P2POp(dist.irecv, inb, peer, fabric.group)]):
+                    w.wait()
+            elif b == 0:  # blocking transport: the zero side sends first
+                fabric._send(out, peer)
+                fabric._recv(inb, peer)
+            else:
+                fabric._recv(inb, peer)
+                fabric._send(out, peer)
+            piece.copy_(inb.view(piece.shape))
+        finally:
+            fabric.scratch.give(inb)
 
 
 def run_circuit_remapped(states, circuit: Circuit, transports, *, fusion=None, restore: bool = True,

@@ -59,6 +59,33 @@ class ShmOracleExecutor:
         oracle.exchange_chunk_raw(state.amps.ctypes.data, buf.data_ptr(), state.layout.m, own_is_zero, c_local,
                                   q.mat, j0, count)
 
+    def pair_update(self, mine, buf, own_is_zero, q):
+        from oracle import oracle
+
+        oracle.exchange_chunk_raw(mine.data_ptr(), buf.data_ptr(), 0, own_is_zero, -1, q.mat, 0, mine.numel())
+
+    def tensor(self, state):
+        import torch
+
+        return torch.from_numpy(state.amps)
+
+    def buffer_device(self, state):
+        import torch
+
+        return torch.device("cpu")
+
+    def ce_exchange(self, state, theirs, own_is_zero, segments, q, bufs):
+        """Copy-engine plane stand-in: partner chunk -> local buffer -> pair update -> back."""
+        from oracle import oracle
+
+        m = state.layout.m
+        w = np.frombuffer((ctypes.c_char * (16 << m)).from_address(theirs), dtype=np.complex128)
+        for i, (j0, cnt, cl) in enumerate(segments):
+            buf = bufs[i % len(bufs)][:cnt]
+            buf.numpy()[:] = w[j0:j0 + cnt]
+            oracle.exchange_chunk_raw(state.amps.ctypes.data, buf.data_ptr(), m, own_is_zero, cl, q.mat, j0, cnt)
+            w[j0:j0 + cnt] = buf.numpy()
+
     def scratch(self, state, num_amps):
         import torch
 
@@ -169,10 +196,10 @@ def _worker(rank, world, port, path, name, n, plane="ipc"):
         state = ShmState(lay, amps, shm)
         ex = ShmOracleExecutor()
         fabric = sv.NvlinkFabric(fence="host", executor=ex, data_plane=plane, chunk_amps=1 << max(0, m - 3))
-        if plane == "nccl":  # the gather below still maps the peers' shared memory
+        if plane != "ipc":  # the gather below maps the peers' shared memory
             fabric.data_plane = "ipc"
             fabric.ensure_registered(state)
-            fabric.data_plane = "nccl"
+            fabric.data_plane = plane
         deltas = []
         for t, c, q in zip(d["t"], d["c"], d["q"]):
             t, c, gate = int(t), None if c < 0 else int(c), sv.GateMatrix.unchecked(q.reshape(2, 2))
@@ -222,17 +249,24 @@ def run_world(world, name, n, golden, plane="ipc"):
         return dict(np.load(path + ".out.npz")), d
 
 
-@pytest.mark.parametrize("world,name,n", [(2, "mix10", 10), (4, "ctl12", 12)])
+@pytest.mark.parametrize("world,name,n", [(2, "mix10", 10), (4, "ctl12", 12), (2, "ctl12", 12)])
 def test_gloo_nccl_data_plane_matches_reference(golden, world, name, n):
-    """The staged send/recv data plane (baseline / fallback) gives the same bits."""
+    """The staged send/recv data plane (baseline / fallback) gives the same bits and, with case 5
+    packed to the bit-c = 1 elements, the reference's own per-gate byte counts -- with chunks
+    smaller than 2^(c+1) for the high controls (chunk = 2^(m-3))."""
     out, d = run_world(world, name, n, golden, plane="nccl")
     p = world.bit_length() - 1
     assert np.array_equal(out["full"], d[f"{name}_p{p}"])
-    m = n - p
-    # bytes: full halves cross for every exchange, packed case-5 traffic included
-    for t, c, _ in unpack_ops(d, name):
-        pass
-    assert out["deltas"].sum() > 0 and m > 0
+    assert np.array_equal(out["deltas"], d[f"{name}_p{p}_bytes"])
+
+
+@pytest.mark.parametrize("world,name,n", [(2, "mix10", 10), (4, "ctl12", 12)])
+def test_gloo_ce_data_plane_matches_reference(golden, world, name, n):
+    """The copy-engine plane's chunk segmentation (skipping chunks on the clear side of a high
+    control bit) gives the same bits as the reference."""
+    out, d = run_world(world, name, n, golden, plane="ce")
+    p = world.bit_length() - 1
+    assert np.array_equal(out["full"], d[f"{name}_p{p}"])
 
 
 @pytest.mark.parametrize("world,name,n", [(2, "mix10", 10), (4, "mix8", 8), (8, "ctl12", 12)])
@@ -406,7 +440,7 @@ def test_gloo_diagonal_local_protocol(world, n):
     assert int(out["fences"]) == 2 * sum(1 for o in glob if o.target >= m) + 1
 
 
-def _worker_remap(rank, world, port, path, n):
+def _worker_remap(rank, world, port, path, n, plane="ipc"):
     """run_circuit_remapped: global<->local swaps instead of per-gate exchanges."""
     import torch.distributed as dist
 
@@ -423,7 +457,7 @@ def _worker_remap(rank, world, port, path, n):
         amps[:] = d["init"][rank << m:(rank + 1) << m]
         state = ShmState(lay, amps, shm)
         ex = ShmOracleExecutor()
-        fabric = sv.NvlinkFabric(fence="host", executor=ex)
+        fabric = sv.NvlinkFabric(fence="host", executor=ex, data_plane=plane, chunk_amps=1 << max(0, m - 4))
         circ = sv.Circuit(n, [sv.GateOp(sv.GateMatrix.unchecked(q.reshape(2, 2)), int(t), None if c < 0 else int(c))
                               for t, c, q in zip(d["t"], d["c"], d["q"])])
         qm = sv.run_circuit_remapped(state, circ, fabric, executor=ex)
@@ -445,8 +479,9 @@ def _worker_remap(rank, world, port, path, n):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,n", [(2, 8), (4, 9), (8, 10)])
-def test_gloo_remapped_execution(world, n):
+@pytest.mark.parametrize("world,n,plane", [(2, 8, "ipc"), (4, 9, "ipc"), (8, 10, "ipc"), (2, 8, "nccl"),
+                                           (4, 9, "nccl")])
+def test_gloo_remapped_execution(world, n, plane):
     """QFT + random gates with global<->local swaps over real ranks: the
     oracle's state, the identity map at the end, and fewer link bytes than the exchanges."""
     import torch.multiprocessing as mp
@@ -468,7 +503,7 @@ def test_gloo_remapped_execution(world, n):
         np.savez(path + ".npz", init=init, t=np.array([o.target for o in circ]),
                  c=np.array([-1 if o.control is None else o.control for o in circ]),
                  q=np.stack([o.gate.mat.reshape(4) for o in circ]))
-        mp.spawn(_worker_remap, args=(world, _port(), path, n), nprocs=world, join=True)
+        mp.spawn(_worker_remap, args=(world, _port(), path, n, plane), nprocs=world, join=True)
         out = dict(np.load(path + ".out.npz"))
     assert np.array_equal(out["full"], want) and bool(out["ident"])
     items, _ = sv.plan_remapped(circ.gates, n, m)
