@@ -436,7 +436,8 @@ def make_units(sv, circ, m, fusion, l_c, state, fabric, remap=False):
 
         tile = tile_for(l_c, m)
         exact = fusion == "passes"
-        return [("pass-" + p.kind, (32 << m) if p.local else (1 << (m + 4)), len(p.gates),
+        return [("pass-" + p.kind + ("_tol" if not p.exact and p.kind == "local_stage" else ""),
+                 (32 << m) if p.local else (1 << (m + 4)), len(p.gates),
                  (lambda p=p: sv.execute_pass(state, p, fabric, tile=tile)), p.gates)
                 for p in sv.plan_passes(circ.gates, m, tile, exact=exact)]
     units = []
@@ -460,7 +461,8 @@ KERNELS = {
     "pass-local_stage": ("sv_apply_gates:stage", "k_mstage (sv_apply_gates, multi-target stage pass)"),
     "pass-local_tile": ("sv_apply_gates:tile", "k_tile (sv_apply_gates, register-tiled run)"),
     "pass-local_gate": ("sv_apply_single", "k_pairs/k_shfl (single gate of a pass plan)"),
-    "pass-local_diag": ("sv_apply_gates:diag", "k_dstage (tolerance mode: collapsed diagonal stages)"),
+    "pass-local_stage_tol": ("sv_apply_gates:dstage", "k_dstage (tolerance mode: diagonal runs folded into "
+                                                      "per-byte product tables, k_dtable)"),
 }
 GLOBAL_KINDS = ("exchange", "swap", "pass-global_stage", "pass-global_gate")
 

@@ -896,6 +896,9 @@ constexpr int MS_N = 1 << MS_K;
 #endif
 constexpr int MS_BLK = SV_MS_BLK;
 constexpr int MS_MAX = SV_MSTAGE_MAX_GATES;
+#ifndef SV_MS_PIPE
+#define SV_MS_PIPE 0  // 1: persistent cp.async-pipelined k_mstage_pipe (measured QFT(30) 107 ms vs 69.4: 512 threads/SM cannot feed FP64)
+#endif
 #ifndef SV_MS_HILANE
 #define SV_MS_HILANE 1  // measured: QFT(30) 72.2 -> 69.5 ms
 #endif
@@ -1123,6 +1126,14 @@ __device__ __noinline__ void ms_replay(double2 *__restrict__ a, uint64_t base, c
 }
 
 
+// Async 16-B global -> shared copies (L2 only): the next group streams in while this one computes.
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
 __global__ void __launch_bounds__(MS_BLK, SV_MS_MINB * 256 / MS_BLK) k_mstage(double2 *__restrict__ a,
                                                                           uint64_t ngroups,
                                                                           const __grid_constant__ MsParams P) {
@@ -1160,6 +1171,73 @@ __global__ void __launch_bounds__(MS_BLK, SV_MS_MINB * 256 / MS_BLK) k_mstage(do
   for (int j = 0; j < MS_N; ++j) a[base | ms_off(j, b)] = r[j];
 }
 
+__device__ __forceinline__ uint64_t ms_base(uint64_t p, const MsParams &P) {
+  uint64_t base = p;
+#if SV_MS_HILANE
+  if (P.hl[0] >= 0) {
+    base = (p & 7ull) | ((p >> 5) << 3);
+    for (int i = 0; i < P.nins; ++i) base = insert_zero(base, P.ins[i]);
+    return base | (((p >> 3) & 1ull) << P.hl[0]) | (((p >> 4) & 1ull) << P.hl[1]);
+  }
+#endif
+#pragma unroll
+  for (int s = 0; s < MS_K; ++s) base = insert_zero(base, P.bits[s]);
+  return base;
+}
+
+// k_mstage, persistent and software-pipelined: group i+1's 16 amplitudes are copied into this
+// thread's shared-memory column (cp.async) while group i is updated in registers, so the HBM
+// reads of the next group overlap the FP64 work of this one (a plain k_mstage thread loads,
+// computes, stores, and its SM's memory pipe idles while its warps compute).  Loop counts are
+// warp-uniform (ngroups and the stride are multiples of 32), so the ballots stay full-warp.
+#ifndef SV_MSP_MINB
+#define SV_MSP_MINB 2  // k_mstage_pipe: threads per SM in units of 256 (register budget)
+#endif
+__global__ void __launch_bounds__(MS_BLK, SV_MSP_MINB * 256 / MS_BLK) k_mstage_pipe(double2 *__restrict__ a,
+                                                                               uint64_t ngroups,
+                                                                               const __grid_constant__ MsParams P) {
+  extern __shared__ double2 ms_smem[];  // [MS_N][MS_BLK]
+  const int tid = threadIdx.x;
+  uint64_t b[MS_K];
+#pragma unroll
+  for (int s = 0; s < MS_K; ++s) b[s] = 1ull << P.bits[s];
+  const uint64_t stride = (uint64_t)gridDim.x * MS_BLK;
+  uint64_t p = (uint64_t)blockIdx.x * MS_BLK + tid;
+  if (p < ngroups) {
+    const uint64_t base = ms_base(p, P);
+#pragma unroll
+    for (int j = 0; j < MS_N; ++j) cp_async16(&ms_smem[j * MS_BLK + tid], a + (base | ms_off(j, b)));
+  }
+  cp_async_commit();
+  for (; p - tid + (tid & ~31) < ngroups; p += stride) {  // warp-uniform trip count
+    const bool live = p < ngroups;
+    const uint64_t base = ms_base(p, P);
+    double2 r[MS_N];
+    cp_async_wait_all();
+#pragma unroll
+    for (int j = 0; j < MS_N; ++j) r[j] = live ? ms_smem[j * MS_BLK + tid] : make_double2(1.0, 1.0);
+    const uint64_t pn = p + stride;
+    if (pn < ngroups) {
+      const uint64_t bn = ms_base(pn, P);
+#pragma unroll
+      for (int j = 0; j < MS_N; ++j) cp_async16(&ms_smem[j * MS_BLK + tid], a + (bn | ms_off(j, b)));
+    }
+    cp_async_commit();
+    ms_run(r, base, P);
+    bool ok = true;
+#pragma unroll
+    for (int j = 0; j < MS_N; ++j) ok &= nonzero2(r[j]);
+    if (!live) continue;
+    if (__builtin_expect(!ok, 0)) {
+      ms_replay(a, base, &P);
+      continue;
+    }
+#pragma unroll
+    for (int j = 0; j < MS_N; ++j) a[base | ms_off(j, b)] = r[j];
+  }
+  cp_async_wait_all();
+}
+
 // ------------------------------------- tolerance-mode stage passes (FusionConfig exact=False)
 //
 // The same thread layout as k_mstage (16 amplitudes spanning four slot bits,
@@ -1187,6 +1265,8 @@ enum { DS_GATE = 0, DS_FLUSH = 2 };
 
 struct DsParams {
   int32_t nops, nbytes;   // nbytes: index bytes a fold table covers (ceil(m / 8))
+  int32_t nfg;            // fold groups
+  uint32_t has0;          // bit g: group g has a d0 != 1 factor (first 32 groups)
   int32_t bits[MS_K];
   const double2 *tab;     // k_dtable output: per group [T1: nbytes x 256][T0: nbytes x 256]
   uint64_t hdr[DS_MAX];   // type 0-1 | slot 2-3 | cmode 4-5 (2: control on a non-slot bit) |
@@ -1223,9 +1303,14 @@ __global__ void __launch_bounds__(256) k_dtable(const __grid_constant__ DtParams
 
 __device__ __forceinline__ double2 cmul2(double2 f, double2 a) { return cmul(f.x, f.y, a); }
 
-__device__ __forceinline__ double2 ds_factor(const double2 *__restrict__ t, int nbytes, uint64_t base) {
-  double2 f = t[base & 255u];
-  for (int k = 1; k < nbytes; ++k) f = cmul2(t[k * 256 + ((base >> (8 * k)) & 255u)], f);
+template <int NB>
+__device__ __forceinline__ double2 ds_factor(const double2 *__restrict__ t, uint64_t base) {
+  double2 e[NB];
+#pragma unroll
+  for (int k = 0; k < NB; ++k) e[k] = t[k * 256 + ((base >> (8 * k)) & 255u)];  // all loads first
+  double2 f = e[0];
+#pragma unroll
+  for (int k = 1; k < NB; ++k) f = cmul2(e[k], f);
   return f;
 }
 
@@ -1263,44 +1348,73 @@ __device__ __forceinline__ void ds_gate(int code, double2 (&r)[MS_N], const doub
 }
 
 #ifndef SV_DS_MINB
-#define SV_DS_MINB 2  // 256-thread CTAs per SM (measured QFT(30) tolerance passes: 2 -> 7.0 ms, 3 -> 7.7, 4 -> 11.0)
+#define SV_DS_MINB 2  // 256-thread CTAs per SM
 #endif
 
+__device__ __forceinline__ uint64_t ds_base(uint64_t p, const int32_t (&bits)[MS_K]) {
+  uint64_t base = p;
+#pragma unroll
+  for (int s = 0; s < MS_K; ++s) base = insert_zero(base, bits[s]);
+  return base;
+}
+
+// Persistent: each thread walks groups p, p + stride, ...; group i+1's 16 amplitudes are copied
+// into this thread's shared-memory slots (cp.async) while group i is updated in registers, so
+// HBM reads stay in flight through the compute.  NB = index bytes of the fold tables.
+template <int NB>
 __global__ void __launch_bounds__(256, SV_DS_MINB) k_dstage(double2 *__restrict__ a, uint64_t ngroups,
                                                            const __grid_constant__ DsParams P) {
-  const uint64_t p = (uint64_t)blockIdx.x * 256 + threadIdx.x;
-  if (p >= ngroups) return;
-  uint64_t b[MS_K], base = p;
+  extern __shared__ double2 stage_smem[];  // [MS_N][256]: this thread's slots are a column
+  double2(*stage)[256] = reinterpret_cast<double2(*)[256]>(stage_smem);
+  const int tid = threadIdx.x;
+  uint64_t b[MS_K];
 #pragma unroll
-  for (int s = 0; s < MS_K; ++s) {
-    b[s] = 1ull << P.bits[s];
-    base = insert_zero(base, P.bits[s]);
+  for (int s = 0; s < MS_K; ++s) b[s] = 1ull << P.bits[s];
+  const uint64_t stride = (uint64_t)gridDim.x * 256;
+  uint64_t p = (uint64_t)blockIdx.x * 256 + tid;
+  if (p < ngroups) {
+    const uint64_t base = ds_base(p, P.bits);
+#pragma unroll
+    for (int j = 0; j < MS_N; ++j) cp_async16(&stage[j][tid], a + (base | ms_off(j, b)));
   }
-  double2 r[MS_N];
+  cp_async_commit();
+  const int nb = NB;
+  for (; p < ngroups; p += stride) {
+    const uint64_t base = ds_base(p, P.bits);
+    double2 r[MS_N];
+    cp_async_wait_all();
 #pragma unroll
-  for (int j = 0; j < MS_N; ++j) r[j] = a[base | ms_off(j, b)];
-  const int nb = P.nbytes;
-  for (int i = 0; i < P.nops; ++i) {
-    const uint64_t h = P.hdr[i];
-    const int s = (int)((h >> 2) & 3u);
-    if ((h & 3u) == DS_FLUSH) {
-      const double2 *t = P.tab + (size_t)((h >> 16) & 0xffu) * 2 * nb * 256;
-      const double2 f1 = ds_factor(t, nb, base);
-      const bool do0 = (h >> 6) & 1u;
-      const double2 f0 = do0 ? ds_factor(t + nb * 256, nb, base) : make_double2(1.0, 0.0);
-      switch (s) {
-        case 0: ds_flush<0>(r, f1, f0, do0); break;
-        case 1: ds_flush<1>(r, f1, f0, do0); break;
-        case 2: ds_flush<2>(r, f1, f0, do0); break;
-        default: ds_flush<MS_K - 1>(r, f1, f0, do0); break;
-      }
-      continue;
+    for (int j = 0; j < MS_N; ++j) r[j] = stage[j][tid];
+    const uint64_t pn = p + stride;
+    if (pn < ngroups) {
+      const uint64_t bn = ds_base(pn, P.bits);
+#pragma unroll
+      for (int j = 0; j < MS_N; ++j) cp_async16(&stage[j][tid], a + (bn | ms_off(j, b)));
     }
-    if (((h >> 4) & 3u) == 2u && !((base >> ((h >> 8) & 63u)) & 1ull)) continue;  // control clear here
-    ds_gate((int)((h >> 16) & 0xffu), r, P.q + (h >> 32));
-  }
+    cp_async_commit();
+    for (int i = 0; i < P.nops; ++i) {
+      const uint64_t h = P.hdr[i];
+      const int s = (int)((h >> 2) & 3u);
+      if ((h & 3u) == DS_FLUSH) {
+        const double2 *t = P.tab + (size_t)((h >> 16) & 0xffu) * 2 * nb * 256;
+        const bool do0 = (h >> 6) & 1u;
+        const double2 f1 = ds_factor<NB>(t, base);
+        const double2 f0 = do0 ? ds_factor<NB>(t + nb * 256, base) : make_double2(1.0, 0.0);
+        switch (s) {
+          case 0: ds_flush<0>(r, f1, f0, do0); break;
+          case 1: ds_flush<1>(r, f1, f0, do0); break;
+          case 2: ds_flush<2>(r, f1, f0, do0); break;
+          default: ds_flush<MS_K - 1>(r, f1, f0, do0); break;
+        }
+        continue;
+      }
+      if (((h >> 4) & 3u) == 2u && !((base >> ((h >> 8) & 63u)) & 1ull)) continue;  // control clear here
+      ds_gate((int)((h >> 16) & 0xffu), r, P.q + (h >> 32));
+    }
 #pragma unroll
-  for (int j = 0; j < MS_N; ++j) a[base | ms_off(j, b)] = r[j];
+    for (int j = 0; j < MS_N; ++j) a[base | ms_off(j, b)] = r[j];
+  }
+  cp_async_wait_all();
 }
 
 // ------------------------------------------------ diagonal gates on a global qubit
@@ -1967,6 +2081,23 @@ int run_mstage(double2 *a, int m, const sv_gate *gates, int n, cudaStream_t st) 
     R.range = (R.hi == 31 ? 0xffffffffu : ((2u << R.hi) - 1u)) & ~((1u << R.lo) - 1u);
   }
   const uint64_t ng = 1ull << (m - MS_K);
+#if SV_MS_PIPE
+  if (ng >= 32) {
+    static int per = 0, nsm = 0;
+    constexpr int SMEM = MS_N * MS_BLK * (int)sizeof(double2);
+    if (!per) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+      cudaFuncSetAttribute(k_mstage_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_mstage_pipe, MS_BLK, SMEM) != cudaSuccess || per < 1)
+        per = 1;
+    }
+    const unsigned grid = (unsigned)std::min<uint64_t>(grid_for(ng, MS_BLK), (uint64_t)nsm * per);
+    k_mstage_pipe<<<grid, MS_BLK, SMEM, st>>>(a, ng, P);
+    return after_launch("k_mstage_pipe");
+  }
+#endif
   k_mstage<<<grid_for(ng, MS_BLK), MS_BLK, 0, st>>>(a, ng, P);
   return after_launch("k_mstage");
 }
@@ -2088,8 +2219,47 @@ int run_dstage(double2 *a, int m, const sv_gate *gates, int n, cudaStream_t st) 
     const int rc = after_launch("k_dtable");
     if (rc != SV_OK) return rc;
   }
+  P.nfg = ngroups;
+  P.has0 = 0;
+  for (int g = 0; g < ngroups; ++g) P.has0 |= has0[g] ? (1u << g) : 0u;
   const uint64_t ng = 1ull << (m - MS_K);
-  k_dstage<<<grid_for(ng, 256), 256, 0, st>>>(a, ng, P);
+  static int per_sm[9] = {};  // resident CTAs per SM of k_dstage<NB> (persistent grid)
+  constexpr int DS_SMEM = MS_N * 256 * (int)sizeof(double2);  // 64 KiB prefetch slots per CTA
+  auto occupancy = [&](auto kern, int nbt) {
+    if (!per_sm[nbt]) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, DS_SMEM);
+      int v = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kern, 256, DS_SMEM) != cudaSuccess || v < 1) v = 1;
+      per_sm[nbt] = v;
+    }
+    return per_sm[nbt];
+  };
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  int per = 1;
+  switch (nbytes) {
+    case 1: per = occupancy(k_dstage<1>, 1); break;
+    case 2: per = occupancy(k_dstage<2>, 2); break;
+    case 3: per = occupancy(k_dstage<3>, 3); break;
+    case 4: per = occupancy(k_dstage<4>, 4); break;
+    case 5: per = occupancy(k_dstage<5>, 5); break;
+    case 6: per = occupancy(k_dstage<6>, 6); break;
+    case 7: per = occupancy(k_dstage<7>, 7); break;
+    default: per = occupancy(k_dstage<8>, 8); break;
+  }
+  const uint64_t need = grid_for(ng, 256);
+  const unsigned grid = (unsigned)std::min<uint64_t>(need, (uint64_t)nsm * per);
+  switch (nbytes) {
+    case 1: k_dstage<1><<<grid, 256, DS_SMEM, st>>>(a, ng, P); break;
+    case 2: k_dstage<2><<<grid, 256, DS_SMEM, st>>>(a, ng, P); break;
+    case 3: k_dstage<3><<<grid, 256, DS_SMEM, st>>>(a, ng, P); break;
+    case 4: k_dstage<4><<<grid, 256, DS_SMEM, st>>>(a, ng, P); break;
+    case 5: k_dstage<5><<<grid, 256, DS_SMEM, st>>>(a, ng, P); break;
+    case 6: k_dstage<6><<<grid, 256, DS_SMEM, st>>>(a, ng, P); break;
+    case 7: k_dstage<7><<<grid, 256, DS_SMEM, st>>>(a, ng, P); break;
+    default: k_dstage<8><<<grid, 256, DS_SMEM, st>>>(a, ng, P); break;
+  }
   return after_launch("k_dstage");
 }
 // ops <= gates + flushes, and every flush follows a fold and precedes a gate (or ends the pass)

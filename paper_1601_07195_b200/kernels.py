@@ -139,8 +139,22 @@ def device_view(amps) -> tuple[int, int]:
     return amps.data_ptr(), m
 
 
+def _strided(amps, fn) -> bool:
+    """A uniformly strided 1-D CUDA view (what the reference's reshape views are): run `fn` on
+    a contiguous copy and write the result back.  Returns False for contiguous inputs."""
+    if isinstance(amps, torch.Tensor) and amps.is_cuda and amps.dim() == 1 and not amps.is_contiguous():
+        tmp = amps.contiguous()
+        fn(tmp)
+        amps.copy_(tmp)
+        return True
+    return False
+
+
 def apply_single_raw(amps, k: int, q, policy: ThreadPolicy = SERIAL) -> None:
-    """In-place single-qubit update on bit k (kernels.py:187-189); no layout checks."""
+    """In-place single-qubit update on bit k (kernels.py:187-189); no layout checks.
+    Uniformly strided 1-D views are accepted (copy-in / copy-out), as the reference's are."""
+    if _strided(amps, lambda t: apply_single_raw(t, k, q, policy)):
+        return
     ptr, m = device_view(amps)
     if not 0 <= k < m:
         raise ValueError(f"qubit {k} out of range for a {m}-qubit slice")
@@ -149,7 +163,9 @@ def apply_single_raw(amps, k: int, q, policy: ThreadPolicy = SERIAL) -> None:
 
 
 def apply_controlled_raw(amps, c: int, t: int, q, policy: ThreadPolicy = SERIAL) -> None:
-    """In-place controlled update, control c / target t (kernels.py:192-196)."""
+    """In-place controlled update, control c / target t (kernels.py:192-196); strided views as above."""
+    if _strided(amps, lambda a: apply_controlled_raw(a, c, t, q, policy)):
+        return
     ptr, m = device_view(amps)
     if c == t:
         raise ValueError(f"control and target must differ, both are {c}")

@@ -114,3 +114,26 @@ def test_max_abs_diff_kernel():
         want = float(np.max(np.abs(a - b)))
         got = sv.max_abs_diff(torch.from_numpy(a).to(DEV), torch.from_numpy(b).to(DEV))
         assert got == pytest.approx(want, rel=1e-15, abs=0)
+
+
+def test_raw_kernels_accept_strided_views():
+    """The reference's *_raw kernels work on uniformly strided numpy views (kernels.py:174-184);
+    here a strided 1-D CUDA view is updated through a contiguous copy, bit for bit."""
+    import torch
+
+    from oracle import oracle
+
+    rng = np.random.default_rng(8)
+    base = rng.standard_normal(512) + 1j * rng.standard_normal(512)
+    dev = torch.from_numpy(base.copy()).to("cuda:0")
+    view = dev[1::2]
+    want = base.copy()
+    q1, q2 = sv.random_unitary(rng), sv.random_unitary(rng)
+    w = want[1::2].copy()
+    oracle.apply_single(w, 4, q1.mat)
+    oracle.apply_controlled(w, 0, 7, q2.mat)
+    want[1::2] = w
+    sv.apply_single_raw(view, 4, q1)
+    sv.apply_controlled_raw(view, 0, 7, q2)
+    torch.cuda.synchronize()
+    assert np.array_equal(dev.cpu().numpy(), want)

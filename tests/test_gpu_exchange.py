@@ -200,7 +200,7 @@ def _ipc_worker(rank, world, port, path, n, plane):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("plane", ["ipc", "nccl"])
+@pytest.mark.parametrize("plane", ["ipc", "nccl", "ce"])
 def test_two_process_ipc_fabric_matches_oracle(plane):
     import torch.multiprocessing as mp
 
@@ -226,3 +226,47 @@ def test_two_process_ipc_fabric_matches_oracle(plane):
     assert int(out["nrec"]) == len(circ)
     assert int(out["sent"]) == int(out["recv"]) > 0
     assert n_exch >= 3
+
+
+@pytest.mark.parametrize("p", [1, 2, 3])
+@pytest.mark.parametrize("fused", [False, True])
+def test_inproc_copy_engine_plane_matches_oracle(p, fused):
+    """data_plane="ce": peer chunks copied in (cudaMemcpyAsync, copy-in stream), updated by the
+    exchange kernel, pushed back (copy-out stream), double-buffered; chunks smaller than
+    2^(c+1) for high local controls; stage exchanges run per gate on this plane."""
+    n = 14
+    m = n - p
+    rng = np.random.default_rng(50 + p)
+    v = random_state(rng, n)
+    circ = sv.build_qft(n)
+    circ.extend(sv.random_circuit(n, 60, np.random.default_rng(p), controlled_fraction=0.5).gates)
+    circ.extend([sv.GateOp(sv.random_unitary(rng), n - 1, control=c) for c in (0, 3, m - 2, m - 1)])
+    want = v.copy()
+    oracle.run_circuit(want, circ.gates, threads=8)
+    sts = [sv.LocalState(sv.Layout(n, p, r), torch.from_numpy(v[r << m:(r + 1) << m].copy()).to(DEV))
+           for r in range(1 << p)]
+    fabs = sv.InprocFabric.group(sts, data_plane="ce", chunk_amps=1 << 6)
+    sv.run_circuit_inproc(sts, circ, fabs, fusion=sv.FusionConfig(l_c=10, passes=True) if fused else None)
+    torch.cuda.synchronize()
+    got = np.concatenate([s.to_numpy() for s in sts])
+    assert np.array_equal(got, want)
+
+
+def test_copy_engine_plane_scratch_accounting():
+    """The staged planes draw their two chunk buffers from the caller's ScratchPool: the
+    reference's high-water bound 2 * chunk * 16 B (distributed.py:161-181)."""
+    n, p = 12, 1
+    m = n - p
+    v = random_state(np.random.default_rng(5), n)
+    sts = [sv.LocalState(sv.Layout(n, p, r), torch.from_numpy(v[r << m:(r + 1) << m].copy()).to(DEV))
+           for r in range(2)]
+    fabs = sv.InprocFabric.group(sts, data_plane="ce", chunk_amps=1 << 20)
+    pool = sv.ScratchPool()
+    q = sv.random_unitary(np.random.default_rng(6))
+    for r in range(2):
+        sv.apply_single_distributed(sts[r], n - 1, q, fabs[r], chunk_amps=1 << 7, scratch=pool)
+    torch.cuda.synchronize()
+    want = v.copy()
+    oracle.apply_single(want, n - 1, q.mat)
+    assert np.array_equal(np.concatenate([s.to_numpy() for s in sts]), want)
+    assert pool.high_water_bytes == 2 * (1 << 7) * 16 and pool.outstanding_bytes == 0
