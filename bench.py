@@ -70,7 +70,8 @@ def parse(argv=None):
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true", help="skip the config 3/4/5 secondary objects")
-    ap.add_argument("--planes", action="store_true", help="N > 1: also time every exchange data plane")
+    ap.add_argument("--no-planes", action="store_true",
+                    help="N > 1: skip timing one global-qubit gate on every exchange data plane (ipc, ce, nccl)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--out", default=None, help="also write the JSON line here")
     return ap.parse_args(argv)
@@ -461,6 +462,8 @@ KERNELS = {
     "pass-local_stage": ("sv_apply_gates:stage", "k_mstage (sv_apply_gates, multi-target stage pass)"),
     "pass-local_tile": ("sv_apply_gates:tile", "k_tile (sv_apply_gates, register-tiled run)"),
     "pass-local_gate": ("sv_apply_single", "k_pairs/k_shfl (single gate of a pass plan)"),
+    "pass-local_low": ("sv_apply_gates:low", "k_dlow (tolerance mode: gates on qubits 0..5, diagonal runs as "
+                                            "64-entry product tables)"),
     "pass-local_stage_tol": ("sv_apply_gates:dstage", "k_dstage (tolerance mode: diagonal runs folded into "
                                                       "per-byte product tables, k_dtable)"),
 }
@@ -686,7 +689,7 @@ def run_ours(args, world, rank, local):
 
     # ------------------------------ N > 1: every exchange data plane on the same box
     planes = None
-    if args.planes and world > 1 and fabric is not None:
+    if not args.no_planes and world > 1 and fabric is not None and fabric.data_plane != "nccl":
         planes = time_planes(sv, torch, dist, state, fabric, n, m, timer, args, p2p)
 
     # ------------------------------ self-check: inverse circuits restore the input

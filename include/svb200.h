@@ -96,6 +96,8 @@ int sv_apply_gates(void *amps, int m, const sv_gate *gates, int ngates, int tile
 /* Slice bits a register tile gathers (its top tile bits; the rest are runs of 2^(tile-8) amplitudes). */
 #define SV_TILE_GATHER 8
 #define SV_GROUP_STAGE 2 /* stage: targets in <= SV_MSTAGE_MAX_TARGETS qubits, 16 amplitudes per thread */
+#define SV_GROUP_LOW 3   /* tolerance mode only: every target in qubits 0..5 (one warp per 64 amplitudes,
+                          * diagonal runs inside the block as one product table) */
 
 /* The planner of sv_apply_gates, exposed (pure host code, no GPU needed):
  * writes the end index and kind of each launch group, returns the number of

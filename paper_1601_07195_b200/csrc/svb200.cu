@@ -241,6 +241,9 @@ __global__ void __launch_bounds__(FusedShape<T>::NT) k_fused(double2 *__restrict
 // Zero tests are integer tests on the bit patterns (ALU pipe, not FP64).
 
 enum { KIND_GENERAL = 0, KIND_DIAG = 1, KIND_PHASE = 2, KIND_REAL = 3, KIND_HSHARE = 4, KIND_COUNT = 5 };
+// Tolerance mode only (k_dstage): a Hadamard-like butterfly a0 + a1, a0 - a1 whose common real
+// factor s is deferred into one per-thread scale applied after the pass.
+constexpr int KIND_HBF = 5;
 
 __device__ __forceinline__ bool nonzero2(double2 v) {
   const int mx = (__double2hiint(v.x) & 0x7fffffff) | __double2loint(v.x);
@@ -306,6 +309,10 @@ __device__ __forceinline__ void spec_pair(double2 &a0, double2 &a1, const double
                                     __dadd_rn(__dmul_rn(q[0], a0.y), __dmul_rn(q[2], a1.y)));
     a1 = make_double2(__dadd_rn(__dmul_rn(q[4], a0.x), __dmul_rn(q[6], a1.x)),
                       __dadd_rn(__dmul_rn(q[4], a0.y), __dmul_rn(q[6], a1.y)));
+    a0 = n0;
+  } else if (KIND == KIND_HBF) {
+    const double2 n0 = make_double2(__dadd_rn(a0.x, a1.x), __dadd_rn(a0.y, a1.y));
+    a1 = make_double2(__dsub_rn(a0.x, a1.x), __dsub_rn(a0.y, a1.y));
     a0 = n0;
   } else {  // KIND_HSHARE
     const double s = q[0];
@@ -896,9 +903,6 @@ constexpr int MS_N = 1 << MS_K;
 #endif
 constexpr int MS_BLK = SV_MS_BLK;
 constexpr int MS_MAX = SV_MSTAGE_MAX_GATES;
-#ifndef SV_MS_PIPE
-#define SV_MS_PIPE 0  // 1: persistent cp.async-pipelined k_mstage_pipe (measured QFT(30) 107 ms vs 69.4: 512 threads/SM cannot feed FP64)
-#endif
 #ifndef SV_MS_HILANE
 #define SV_MS_HILANE 1  // measured: QFT(30) 72.2 -> 69.5 ms
 #endif
@@ -1171,73 +1175,6 @@ __global__ void __launch_bounds__(MS_BLK, SV_MS_MINB * 256 / MS_BLK) k_mstage(do
   for (int j = 0; j < MS_N; ++j) a[base | ms_off(j, b)] = r[j];
 }
 
-__device__ __forceinline__ uint64_t ms_base(uint64_t p, const MsParams &P) {
-  uint64_t base = p;
-#if SV_MS_HILANE
-  if (P.hl[0] >= 0) {
-    base = (p & 7ull) | ((p >> 5) << 3);
-    for (int i = 0; i < P.nins; ++i) base = insert_zero(base, P.ins[i]);
-    return base | (((p >> 3) & 1ull) << P.hl[0]) | (((p >> 4) & 1ull) << P.hl[1]);
-  }
-#endif
-#pragma unroll
-  for (int s = 0; s < MS_K; ++s) base = insert_zero(base, P.bits[s]);
-  return base;
-}
-
-// k_mstage, persistent and software-pipelined: group i+1's 16 amplitudes are copied into this
-// thread's shared-memory column (cp.async) while group i is updated in registers, so the HBM
-// reads of the next group overlap the FP64 work of this one (a plain k_mstage thread loads,
-// computes, stores, and its SM's memory pipe idles while its warps compute).  Loop counts are
-// warp-uniform (ngroups and the stride are multiples of 32), so the ballots stay full-warp.
-#ifndef SV_MSP_MINB
-#define SV_MSP_MINB 2  // k_mstage_pipe: threads per SM in units of 256 (register budget)
-#endif
-__global__ void __launch_bounds__(MS_BLK, SV_MSP_MINB * 256 / MS_BLK) k_mstage_pipe(double2 *__restrict__ a,
-                                                                               uint64_t ngroups,
-                                                                               const __grid_constant__ MsParams P) {
-  extern __shared__ double2 ms_smem[];  // [MS_N][MS_BLK]
-  const int tid = threadIdx.x;
-  uint64_t b[MS_K];
-#pragma unroll
-  for (int s = 0; s < MS_K; ++s) b[s] = 1ull << P.bits[s];
-  const uint64_t stride = (uint64_t)gridDim.x * MS_BLK;
-  uint64_t p = (uint64_t)blockIdx.x * MS_BLK + tid;
-  if (p < ngroups) {
-    const uint64_t base = ms_base(p, P);
-#pragma unroll
-    for (int j = 0; j < MS_N; ++j) cp_async16(&ms_smem[j * MS_BLK + tid], a + (base | ms_off(j, b)));
-  }
-  cp_async_commit();
-  for (; p - tid + (tid & ~31) < ngroups; p += stride) {  // warp-uniform trip count
-    const bool live = p < ngroups;
-    const uint64_t base = ms_base(p, P);
-    double2 r[MS_N];
-    cp_async_wait_all();
-#pragma unroll
-    for (int j = 0; j < MS_N; ++j) r[j] = live ? ms_smem[j * MS_BLK + tid] : make_double2(1.0, 1.0);
-    const uint64_t pn = p + stride;
-    if (pn < ngroups) {
-      const uint64_t bn = ms_base(pn, P);
-#pragma unroll
-      for (int j = 0; j < MS_N; ++j) cp_async16(&ms_smem[j * MS_BLK + tid], a + (bn | ms_off(j, b)));
-    }
-    cp_async_commit();
-    ms_run(r, base, P);
-    bool ok = true;
-#pragma unroll
-    for (int j = 0; j < MS_N; ++j) ok &= nonzero2(r[j]);
-    if (!live) continue;
-    if (__builtin_expect(!ok, 0)) {
-      ms_replay(a, base, &P);
-      continue;
-    }
-#pragma unroll
-    for (int j = 0; j < MS_N; ++j) a[base | ms_off(j, b)] = r[j];
-  }
-  cp_async_wait_all();
-}
-
 // ------------------------------------- tolerance-mode stage passes (FusionConfig exact=False)
 //
 // The same thread layout as k_mstage (16 amplitudes spanning four slot bits,
@@ -1267,6 +1204,7 @@ struct DsParams {
   int32_t nops, nbytes;   // nbytes: index bytes a fold table covers (ceil(m / 8))
   int32_t nfg;            // fold groups
   uint32_t has0;          // bit g: group g has a d0 != 1 factor (first 32 groups)
+  double scale;           // product of the deferred butterfly factors (KIND_HBF)
   int32_t bits[MS_K];
   const double2 *tab;     // k_dtable output: per group [T1: nbytes x 256][T0: nbytes x 256]
   uint64_t hdr[DS_MAX];   // type 0-1 | slot 2-3 | cmode 4-5 (2: control on a non-slot bit) |
@@ -1340,6 +1278,7 @@ __device__ __forceinline__ void ds_gate(int code, double2 (&r)[MS_N], const doub
 #define DS_CASES(K_) DS_CASES_S(K_, 0) DS_CASES_S(K_, 1) DS_CASES_S(K_, 2) DS_CASES_S(K_, 3)
 #endif
     DS_CASES(KIND_GENERAL) DS_CASES(KIND_DIAG) DS_CASES(KIND_PHASE) DS_CASES(KIND_REAL) DS_CASES(KIND_HSHARE)
+    DS_CASES(KIND_HBF)
 #undef DS_CASES
 #undef DS_CASES_S
 #undef DS_CASE
@@ -1349,6 +1288,12 @@ __device__ __forceinline__ void ds_gate(int code, double2 (&r)[MS_N], const doub
 
 #ifndef SV_DS_MINB
 #define SV_DS_MINB 2  // 256-thread CTAs per SM
+#endif
+#ifndef SV_DS_GRAY
+#define SV_DS_GRAY 1  // element addresses in Gray-code order (one XOR each)
+#endif
+#ifndef SV_DS_HBF
+#define SV_DS_HBF 1  // uncontrolled Hadamard-like gates as unscaled butterflies, factor applied once
 #endif
 
 __device__ __forceinline__ uint64_t ds_base(uint64_t p, const int32_t (&bits)[MS_K]) {
@@ -1372,11 +1317,21 @@ __global__ void __launch_bounds__(256, SV_DS_MINB) k_dstage(double2 *__restrict_
   for (int s = 0; s < MS_K; ++s) b[s] = 1ull << P.bits[s];
   const uint64_t stride = (uint64_t)gridDim.x * 256;
   uint64_t p = (uint64_t)blockIdx.x * 256 + tid;
-  if (p < ngroups) {
-    const uint64_t base = ds_base(p, P.bits);
-#pragma unroll
-    for (int j = 0; j < MS_N; ++j) cp_async16(&stage[j][tid], a + (base | ms_off(j, b)));
+  // the 16 elements of a group in Gray-code order: one XOR per address (base has zeros at the slots)
+#define DS_GRAY(BASE, BODY)                                                                   \
+  {                                                                                           \
+    uint64_t ix = (BASE);                                                                     \
+    _Pragma("unroll") for (int i = 0; i < MS_N; ++i) {                                        \
+      const int j = i ^ (i >> 1);                                                             \
+      if (SV_DS_GRAY) {                                                                       \
+        if (i) ix ^= b[(i & 1) ? 0 : (i & 2) ? 1 : (i & 4) ? 2 : MS_K - 1];                    \
+      } else {                                                                                \
+        ix = (BASE) | ms_off(j, b);                                                           \
+      }                                                                                       \
+      BODY;                                                                                   \
+    }                                                                                         \
   }
+  if (p < ngroups) DS_GRAY(ds_base(p, P.bits), cp_async16(&stage[j][tid], a + ix));
   cp_async_commit();
   const int nb = NB;
   for (; p < ngroups; p += stride) {
@@ -1386,11 +1341,7 @@ __global__ void __launch_bounds__(256, SV_DS_MINB) k_dstage(double2 *__restrict_
 #pragma unroll
     for (int j = 0; j < MS_N; ++j) r[j] = stage[j][tid];
     const uint64_t pn = p + stride;
-    if (pn < ngroups) {
-      const uint64_t bn = ds_base(pn, P.bits);
-#pragma unroll
-      for (int j = 0; j < MS_N; ++j) cp_async16(&stage[j][tid], a + (bn | ms_off(j, b)));
-    }
+    if (pn < ngroups) DS_GRAY(ds_base(pn, P.bits), cp_async16(&stage[j][tid], a + ix));
     cp_async_commit();
     for (int i = 0; i < P.nops; ++i) {
       const uint64_t h = P.hdr[i];
@@ -1411,10 +1362,148 @@ __global__ void __launch_bounds__(256, SV_DS_MINB) k_dstage(double2 *__restrict_
       if (((h >> 4) & 3u) == 2u && !((base >> ((h >> 8) & 63u)) & 1ull)) continue;  // control clear here
       ds_gate((int)((h >> 16) & 0xffu), r, P.q + (h >> 32));
     }
+    if (P.scale != 1.0) {  // the deferred Hadamard factors
+      const double sc = P.scale;
 #pragma unroll
-    for (int j = 0; j < MS_N; ++j) a[base | ms_off(j, b)] = r[j];
+      for (int j = 0; j < MS_N; ++j) r[j] = make_double2(r[j].x * sc, r[j].y * sc);
+    }
+    DS_GRAY(base, a[ix] = r[j]);
   }
+#undef DS_GRAY
   cp_async_wait_all();
+}
+
+// ------------------------------ tolerance-mode low-bit passes (targets in slice bits 0..5)
+//
+// One warp per 256-amplitude block (slice bits 0..7); each lane holds 8 elements in one of
+// two layouts: H -- registers on bits 3, 4, 5, lanes on bits 0, 1, 2, 6, 7; L -- registers
+// on bits 0, 1, 2, lanes on bits 3..7.  Every gate's target is a register bit of the
+// current layout (the host inserts a layout switch -- a transpose through the warp's
+// XOR-swizzled shared memory -- when needed), so updates never shuffle.  A run of diagonal
+// gates whose target and control lie in bits 0..5 (a transform stage's R(k, c) for all
+// c < k <= 5) is ONE 64-entry product table (built on the host): one complex multiply per
+// element.  Uncontrolled Hadamard-like gates run as unscaled butterflies with their factor
+// applied once at the end.  Controls: register bits -> pair predicates, lane bits (incl.
+// 6, 7) -> lane predicates, bits >= 8 -> warp-uniform.  Values equal the reference's within
+// rounding (FusionConfig exact=False).
+
+constexpr int DL_BITS = 6, DL_MAX = 96, DL_TABMAX = 12;
+enum { DL_GATE = 0, DL_TABLE = 1, DL_LAYOUT = 2 };
+
+struct DlParams {
+  int32_t nops, ntab;
+  double scale;  // deferred butterfly factors
+  uint64_t hdr[2 * DL_MAX + DL_TABMAX];  // type 0-1 | register bit 2-3 | kind 4-7 | cmode 8-9 (0 none,
+                                         // 1 register bit, 2 lane-or-above bit) | cbit 10-15 (register
+                                         // bit or slice bit) | index 16-31 (gate, table; layout: 0 H, 1 L)
+  double q[DL_MAX][8];
+  double2 tab[DL_TABMAX][64];
+};
+
+__device__ __forceinline__ int dl_x(int layout, int lane, int j) {  // slice bits 0..7 of (lane, reg j)
+  return layout ? (j | (lane << 3)) : ((lane & 7) | (j << 3) | ((lane >> 3) << 6));
+}
+__device__ __forceinline__ int dl_swz(int x) { return x ^ ((x >> 3) & 7); }
+
+template <int RB, int KIND>
+__device__ __forceinline__ void dl_gate(double2 (&r)[8], uint32_t pm, const double *q) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int j = ((k >> RB) << (RB + 1)) | (k & ((1 << RB) - 1));
+    if ((pm >> j) & 1u) spec_pair<KIND>(r[j], r[j | (1 << RB)], q);
+  }
+}
+
+template <int LAYOUT>
+__device__ __forceinline__ void dl_table(double2 (&r)[8], const double2 *__restrict__ t, int lane) {
+  // layout H: x & 63 = (lane & 7) | (j << 3); layout L: (lane << 3 | j) & 63 -- one base, 8 immediates
+  const double2 *tb = t + (LAYOUT ? ((lane << 3) & 63) : (lane & 7));
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = cmul2(tb[LAYOUT ? j : (j << 3)], r[j]);
+}
+
+template <int FROM>
+__device__ __forceinline__ void dl_transpose(double2 (&r)[8], double2 *buf, int lane) {
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < 8; ++j) buf[dl_swz(dl_x(FROM, lane, j))] = r[j];
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = buf[dl_swz(dl_x(1 - FROM, lane, j))];
+}
+
+__global__ void __launch_bounds__(256, 3) k_dlow(double2 *__restrict__ a, uint64_t nblocks,
+                                                 const __grid_constant__ DlParams P) {
+  __shared__ double2 tab[DL_TABMAX * 64];
+  __shared__ double2 xp[8][256];  // one 4 KiB transpose buffer per warp
+  for (int i = threadIdx.x; i < P.ntab * 64; i += 256) tab[i] = P.tab[i >> 6][i & 63];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double2 *buf = xp[w];
+  const uint64_t nw = (uint64_t)gridDim.x * 8;
+  uint64_t blk = (uint64_t)blockIdx.x * 8 + w;
+  if (blk >= nblocks) return;
+  double2 nx[8];  // the next block's elements, loaded before this block's gates
+#pragma unroll
+  for (int j = 0; j < 8; ++j) nx[j] = a[(blk << 8) + dl_x(0, lane, j)];
+  for (; blk < nblocks; blk += nw) {
+    const uint64_t base = blk << 8;
+    double2 r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = nx[j];
+    if (blk + nw < nblocks) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) nx[j] = a[((blk + nw) << 8) + dl_x(0, lane, j)];
+    }
+    int layout = 0;
+    for (int i = 0; i < P.nops; ++i) {
+      const uint64_t h = P.hdr[i];
+      const int type = (int)(h & 3u), idx = (int)((h >> 16) & 0xffffu);
+      if (type == DL_LAYOUT) {
+        if (layout)
+          dl_transpose<1>(r, buf, lane);
+        else
+          dl_transpose<0>(r, buf, lane);
+        layout = idx;
+        continue;
+      }
+      if (type == DL_TABLE) {
+        if (layout)
+          dl_table<1>(r, tab + idx * 64, lane);
+        else
+          dl_table<0>(r, tab + idx * 64, lane);
+        continue;
+      }
+      const int cmode = (int)((h >> 8) & 3u), cbit = (int)((h >> 10) & 63u);
+      uint32_t pm = 0xffu;
+      if (cmode == 1) {
+        pm = cbit == 0 ? 0xAAu : cbit == 1 ? 0xCCu : 0xF0u;  // registers whose bit cbit is set
+      } else if (cmode == 2) {
+        const int x0 = dl_x(layout, lane, 0);  // this lane's bits; cbit is not a register bit here
+        const bool on = cbit < 8 ? ((x0 >> cbit) & 1) : ((base >> cbit) & 1ull);
+        if (!on) continue;
+      }
+      const double *q = P.q[idx];
+      const int rb = (int)((h >> 2) & 3u), kind = (int)((h >> 4) & 15u);
+      switch (rb * 8 + kind) {
+#define DL_CASE(RB_, K_) \
+  case (RB_)*8 + (K_): dl_gate<RB_, K_>(r, pm, q); break;
+#define DL_KINDS(RB_) DL_CASE(RB_, KIND_GENERAL) DL_CASE(RB_, KIND_DIAG) DL_CASE(RB_, KIND_PHASE) \
+  DL_CASE(RB_, KIND_REAL) DL_CASE(RB_, KIND_HSHARE) DL_CASE(RB_, KIND_HBF)
+        DL_KINDS(0) DL_KINDS(1) DL_KINDS(2)
+#undef DL_KINDS
+#undef DL_CASE
+        default: break;
+      }
+    }
+    if (P.scale != 1.0) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = make_double2(r[j].x * P.scale, r[j].y * P.scale);
+    }
+    if (layout) dl_transpose<1>(r, buf, lane);  // back to layout H for the store
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a[base + dl_x(0, lane, j)] = r[j];
+  }
 }
 
 // ------------------------------------------------ diagonal gates on a global qubit
@@ -2081,23 +2170,6 @@ int run_mstage(double2 *a, int m, const sv_gate *gates, int n, cudaStream_t st) 
     R.range = (R.hi == 31 ? 0xffffffffu : ((2u << R.hi) - 1u)) & ~((1u << R.lo) - 1u);
   }
   const uint64_t ng = 1ull << (m - MS_K);
-#if SV_MS_PIPE
-  if (ng >= 32) {
-    static int per = 0, nsm = 0;
-    constexpr int SMEM = MS_N * MS_BLK * (int)sizeof(double2);
-    if (!per) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-      cudaFuncSetAttribute(k_mstage_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_mstage_pipe, MS_BLK, SMEM) != cudaSuccess || per < 1)
-        per = 1;
-    }
-    const unsigned grid = (unsigned)std::min<uint64_t>(grid_for(ng, MS_BLK), (uint64_t)nsm * per);
-    k_mstage_pipe<<<grid, MS_BLK, SMEM, st>>>(a, ng, P);
-    return after_launch("k_mstage_pipe");
-  }
-#endif
   k_mstage<<<grid_for(ng, MS_BLK), MS_BLK, 0, st>>>(a, ng, P);
   return after_launch("k_mstage");
 }
@@ -2161,6 +2233,7 @@ int run_dstage(double2 *a, int m, const sv_gate *gates, int n, cudaStream_t st) 
   };
   const int nbytes = (m + 7) / 8;
   int nops = 0, nq = 0, ngroups = 0;
+  double scale = 1.0;
   int open_group[MS_K];
   bool has0[DS_MAXG] = {};
   for (int s = 0; s < MS_K; ++s) open_group[s] = -1;
@@ -2199,7 +2272,11 @@ int run_dstage(double2 *a, int m, const sv_gate *gates, int n, cudaStream_t st) 
       continue;
     }
     if (!diag && open_group[s] >= 0) flush(s);
-    const int code = (kind * MS_K + s) * (MS_K + 1) + cs;
+    // an uncontrolled Hadamard-like gate: unscaled butterfly, its real factor deferred to one
+    // multiply of every amplitude after the pass (it applies to all of them)
+    const bool hbf = SV_DS_HBF && kind == KIND_HSHARE && c < 0;
+    if (hbf) scale *= g.q[0];
+    const int code = ((hbf ? KIND_HBF : kind) * MS_K + s) * (MS_K + 1) + cs;
     const uint64_t cm = (c >= 0 && cs == MS_K) ? (2ull << 4) | ((uint64_t)(c & 63) << 8) : 0ull;
     emit((uint64_t)DS_GATE | ((uint64_t)s << 2) | cm | ((uint64_t)code << 16), g.q, 8);
   }
@@ -2220,6 +2297,7 @@ int run_dstage(double2 *a, int m, const sv_gate *gates, int n, cudaStream_t st) 
     if (rc != SV_OK) return rc;
   }
   P.nfg = ngroups;
+  P.scale = scale;
   P.has0 = 0;
   for (int g = 0; g < ngroups; ++g) P.has0 |= has0[g] ? (1u << g) : 0u;
   const uint64_t ng = 1ull << (m - MS_K);
@@ -2266,6 +2344,85 @@ int run_dstage(double2 *a, int m, const sv_gate *gates, int n, cudaStream_t st) 
 static_assert(DS_MAX >= 3 * MS_MAX / 2 + MS_K && DS_QMAX >= 8 * MS_MAX, "k_dstage program capacity");
 static_assert(DT_SLOT_BYTES >= (size_t)DS_MAXG * 2 * ((62 + 7) / 8) * 256 * sizeof(double2), "fold-table slot");
 
+// Tolerance-mode low-bit launch (k_dlow): every target in slice bits 0..5 (controls anywhere).
+int run_dlow(double2 *a, int m, const sv_gate *gates, int n, cudaStream_t st) {
+  static thread_local DlParams P;
+  if (m < 11) return fail(SV_EINVAL, "low-bit group: m=%d below 11", m);
+  if (n < 1 || n > DL_MAX) return fail(SV_EINVAL, "low-bit group: %d gates not in [1, %d]", n, DL_MAX);
+  int nops = 0, ntab = 0, ngate = 0, layout = 0;
+  double scale = 1.0;
+  bool pending = false;
+  double tr[64], ti[64];
+  auto reset = [&]() {
+    for (int x = 0; x < 64; ++x) tr[x] = 1.0, ti[x] = 0.0;
+  };
+  auto flush = [&]() {
+    if (!pending) return 0;
+    if (ntab == DL_TABMAX) return fail(SV_EINVAL, "low-bit group: more than %d diagonal runs", DL_TABMAX);
+    for (int x = 0; x < 64; ++x) P.tab[ntab][x] = make_double2(tr[x], ti[x]);
+    P.hdr[nops++] = (uint64_t)DL_TABLE | ((uint64_t)ntab << 16);
+    ++ntab;
+    pending = false;
+    reset();
+    return 0;
+  };
+  // register bits of a slice bit (< 6) in a layout, -1 when it is a lane bit
+  auto regbit = [](int lay, int b) { return lay ? (b < 3 ? b : -1) : ((b >= 3 && b < 6) ? b - 3 : -1); };
+  reset();
+  for (int k = 0; k < n; ++k) {
+    const sv_gate &g = gates[k];
+    if (g.target < 0 || g.target >= DL_BITS) return fail(SV_EINVAL, "low-bit group: target %d >= %d", g.target, DL_BITS);
+    const int c = g.control, kind = gate_kind(g.q);
+    const bool diag = kind == KIND_DIAG || kind == KIND_PHASE;
+    if (diag && c < DL_BITS) {  // into the block's product table
+      for (int x = 0; x < 64; ++x) {
+        if (c >= 0 && !((x >> c) & 1)) continue;
+        const int o = ((x >> g.target) & 1) ? 6 : 0;
+        const double dr = g.q[o], di = g.q[o + 1];
+        const double nr = tr[x] * dr - ti[x] * di, ni = tr[x] * di + ti[x] * dr;
+        tr[x] = nr;
+        ti[x] = ni;
+      }
+      pending = true;
+      continue;
+    }
+    int rc = flush();
+    if (rc) return rc;
+    if (regbit(layout, g.target) < 0) {  // bring the target into the registers
+      layout ^= 1;
+      P.hdr[nops++] = (uint64_t)DL_LAYOUT | ((uint64_t)layout << 16);
+    }
+    const bool hbf = kind == KIND_HSHARE && c < 0;
+    if (hbf) scale *= g.q[0];
+    uint64_t cm = 0, cb = 0;
+    if (c >= 0) {
+      const int rbc = c < DL_BITS ? regbit(layout, c) : -1;
+      cm = rbc >= 0 ? 1 : 2;
+      cb = rbc >= 0 ? (uint64_t)rbc : (uint64_t)c;
+    }
+    P.hdr[nops++] = (uint64_t)DL_GATE | ((uint64_t)regbit(layout, g.target) << 2) |
+                    ((uint64_t)(hbf ? KIND_HBF : kind) << 4) | (cm << 8) | (cb << 10) | ((uint64_t)ngate << 16);
+    memcpy(P.q[ngate], g.q, sizeof(P.q[0]));
+    ++ngate;
+  }
+  int rc = flush();
+  if (rc) return rc;
+  P.nops = nops;
+  P.ntab = ntab;
+  P.scale = scale;
+  const uint64_t nblocks = 1ull << (m - 8);
+  static int per = 0, nsm = 0;
+  if (!per) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_dlow, 256, 0) != cudaSuccess || per < 1) per = 1;
+  }
+  const unsigned grid = (unsigned)std::min<uint64_t>(grid_for(nblocks, 8), (uint64_t)nsm * per);
+  k_dlow<<<grid, 256, 0, st>>>(a, nblocks, P);
+  return after_launch("k_dlow");
+}
+
 // Native pass planner: the launch group starting at gates[i], returned as its end.
 // Candidate 1, a register-tiled run: targets below L = T-G, or one of up to G
 // (TG_BITS) higher slice bits taken in order of appearance (the tile then
@@ -2287,6 +2444,25 @@ double stage_cost(const sv_gate &g, bool tol) {
   // tolerance mode: a diagonal gate folds into a per-thread factor (one multiply per 16 amplitudes)
   if (tol && (k == KIND_DIAG || k == KIND_PHASE)) return 0.02;
   return c[k] * (g.control >= 0 ? 0.5 : 1.0);
+}
+
+// Tolerance mode: the run from i whose targets all lie in slice bits 0..DL_BITS-1 (k_dlow), as
+// long as its diagonal runs fit the table budget; its length.
+int low_run(int m, const sv_gate *gates, int n, int i) {
+  if (m < 11) return 0;
+  int j = i, tabs = 0;
+  bool in_diag = false;
+  for (; j < n && j - i < DL_MAX; ++j) {
+    if (gates[j].target >= DL_BITS) break;
+    const int k = gate_kind(gates[j].q);
+    const bool d = (k == KIND_DIAG || k == KIND_PHASE) && gates[j].control < DL_BITS;
+    if (d && !in_diag) {
+      if (tabs == DL_TABMAX) break;
+      ++tabs;
+    }
+    in_diag = d;
+  }
+  return j - i;
 }
 
 int next_group(int m, const sv_gate *gates, int n, int i, int T, int *kind, bool tol = false) {
@@ -2328,6 +2504,13 @@ int next_group(int m, const sv_gate *gates, int n, int i, int T, int *kind, bool
   int lowest = 64;
   for (int k = 0; k < ns; ++k) lowest = S[k] < lowest ? S[k] : lowest;
   if (lowest < 3) cs = 1.7 * pass(cs);  // slot bits 0..2: 16-B pieces at 128-B strides per load (measured)
+  if (tol) {  // a low-bit run at least as long as both other candidates: one k_dlow pass
+    const int C = low_run(m, gates, n, i);
+    if (C >= 2 && C >= A && C >= B) {
+      *kind = SV_GROUP_LOW;
+      return i + C;
+    }
+  }
   if (A <= 1 && B <= 1) {
     *kind = SV_GROUP_GATES;
     return i + 1;
@@ -2351,6 +2534,10 @@ int next_group(int m, const sv_gate *gates, int n, int i, int T, int *kind, bool
 }
 
 int exec_group(double2 *a, int m, int T, int kind, const sv_gate *gates, int n, cudaStream_t st, bool tol = false) {
+  if (kind == SV_GROUP_LOW) {
+    if (!tol) return fail(SV_EINVAL, "low-bit groups run in the tolerance mode only (SV_FLAG_TOLERANCE)");
+    return run_dlow(a, m, gates, n, st);
+  }
   if (kind == SV_GROUP_STAGE) {
     if (n == 1) return launch_gate(a, m, gates[0], st);
     return tol ? run_dstage(a, m, gates, n, st) : run_mstage(a, m, gates, n, st);
@@ -2534,7 +2721,7 @@ int sv_apply_group_ex(void *amps, int m, int kind, const sv_gate *gates, int nga
   if (rc != SV_OK) return rc;
   const int tmax = m < SV_FUSED_MAX_TILE ? m : SV_FUSED_MAX_TILE;
   if (tile != 0 && (tile < 9 || tile > tmax)) return fail(SV_EINVAL, "sv_apply_group: tile %d not in [9, %d]", tile, tmax);
-  if (kind < SV_GROUP_GATES || kind > SV_GROUP_STAGE) return fail(SV_EINVAL, "sv_apply_group: kind %d", kind);
+  if (kind < SV_GROUP_GATES || kind > SV_GROUP_LOW) return fail(SV_EINVAL, "sv_apply_group: kind %d", kind);
   return exec_group((double2 *)amps, m, tile > 0 ? tile : tmax, kind, gates, ngates, (cudaStream_t)stream,
                     flags & SV_FLAG_TOLERANCE);
 }

@@ -48,12 +48,12 @@ from .errors import LayoutError, TransportError
 from .kernels import GateMatrix, _as_gate
 
 
-LOCAL_KINDS = ("local_tile", "local_stage", "local_gate")
+LOCAL_KINDS = ("local_tile", "local_stage", "local_gate", "local_low")
 
 
 @dataclass(frozen=True)
 class Pass:
-    kind: str                # local_tile | local_stage | local_gate | global_stage | global_gate
+    kind: str                # local_tile | local_stage | local_gate | local_low (tolerance) | global_*
     gates: tuple[GateOp, ...]
     target: int | None = None
     exact: bool = True       # False: tolerance mode (stage passes through k_dstage)
@@ -113,7 +113,7 @@ def plan_passes(gates, m: int, tile: int = 0, exact: bool = True) -> list[Pass]:
 
 
 _GROUP_KIND = {_lib.SV_GROUP_GATES: "local_gate", _lib.SV_GROUP_TILE: "local_tile",
-               _lib.SV_GROUP_STAGE: "local_stage"}
+               _lib.SV_GROUP_STAGE: "local_stage", _lib.SV_GROUP_LOW: "local_low"}
 _KIND_GROUP = {v: k for k, v in _GROUP_KIND.items()}
 
 
