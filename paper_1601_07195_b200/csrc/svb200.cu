@@ -1414,12 +1414,17 @@ __device__ __forceinline__ void dl_gate(double2 (&r)[8], uint32_t pm, const doub
   }
 }
 
+#ifndef SV_DL_PREFETCH
+#define SV_DL_PREFETCH 1  // k_dlow: the next block's elements load before this block's gates
+#endif
+
 template <int LAYOUT>
 __device__ __forceinline__ void dl_table(double2 (&r)[8], const double2 *__restrict__ t, int lane) {
-  // layout H: x & 63 = (lane & 7) | (j << 3); layout L: (lane << 3 | j) & 63 -- one base, 8 immediates
-  const double2 *tb = t + (LAYOUT ? ((lane << 3) & 63) : (lane & 7));
+  // tables are stored XOR-swizzled (entry x at dl_swz(x)): layout H reads x = (lane & 7) | (j << 3),
+  // layout L x = ((lane & 7) << 3) | j; either way a quarter warp hits 8 distinct 16-B columns
+  const int l7 = lane & 7;
 #pragma unroll
-  for (int j = 0; j < 8; ++j) r[j] = cmul2(tb[LAYOUT ? j : (j << 3)], r[j]);
+  for (int j = 0; j < 8; ++j) r[j] = cmul2(t[LAYOUT ? ((l7 << 3) | (j ^ l7)) : ((j << 3) | (l7 ^ j))], r[j]);
 }
 
 template <int FROM>
@@ -1436,25 +1441,32 @@ __global__ void __launch_bounds__(256, 3) k_dlow(double2 *__restrict__ a, uint64
                                                  const __grid_constant__ DlParams P) {
   __shared__ double2 tab[DL_TABMAX * 64];
   __shared__ double2 xp[8][256];  // one 4 KiB transpose buffer per warp
-  for (int i = threadIdx.x; i < P.ntab * 64; i += 256) tab[i] = P.tab[i >> 6][i & 63];
+  for (int i = threadIdx.x; i < P.ntab * 64; i += 256) tab[(i & ~63) | dl_swz(i & 63)] = P.tab[i >> 6][i & 63];
   __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   double2 *buf = xp[w];
   const uint64_t nw = (uint64_t)gridDim.x * 8;
   uint64_t blk = (uint64_t)blockIdx.x * 8 + w;
   if (blk >= nblocks) return;
+#if SV_DL_PREFETCH
   double2 nx[8];  // the next block's elements, loaded before this block's gates
 #pragma unroll
   for (int j = 0; j < 8; ++j) nx[j] = a[(blk << 8) + dl_x(0, lane, j)];
+#endif
   for (; blk < nblocks; blk += nw) {
     const uint64_t base = blk << 8;
     double2 r[8];
+#if SV_DL_PREFETCH
 #pragma unroll
     for (int j = 0; j < 8; ++j) r[j] = nx[j];
     if (blk + nw < nblocks) {
 #pragma unroll
       for (int j = 0; j < 8; ++j) nx[j] = a[((blk + nw) << 8) + dl_x(0, lane, j)];
     }
+#else
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = a[base + dl_x(0, lane, j)];
+#endif
     int layout = 0;
     for (int i = 0; i < P.nops; ++i) {
       const uint64_t h = P.hdr[i];
