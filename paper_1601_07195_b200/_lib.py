@@ -22,7 +22,7 @@ SV_NORM_SCRATCH = 1025
 SV_STAGE_MAX_GATES = 64
 SV_MSTAGE_MAX_GATES, SV_MSTAGE_MAX_TARGETS = 128, 4
 SV_TILE_GATHER = 8
-SV_GROUP_GATES, SV_GROUP_TILE, SV_GROUP_STAGE, SV_GROUP_LOW = 0, 1, 2, 3
+SV_GROUP_GATES, SV_GROUP_TILE, SV_GROUP_STAGE, SV_GROUP_LOW, SV_GROUP_STAGE2 = 0, 1, 2, 3, 4
 SV_FLAG_TOLERANCE = 1
 ABI_VERSION = 1
 

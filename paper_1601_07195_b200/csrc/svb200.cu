@@ -1219,10 +1219,12 @@ struct DtFold {
   double d[4];      // d0 re, im, d1 re, im
 };
 
+constexpr int DT_MAXF = 2 * MS_MAX;  // folded gates per launch (two phases of k_dstage2)
+
 struct DtParams {
   int32_t nfold, nbytes;
   double2 *tab;
-  DtFold f[MS_MAX];
+  DtFold f[DT_MAXF];
 };
 
 // One block per (group, index byte, table kind); thread v = the byte's value.
@@ -1370,6 +1372,123 @@ __global__ void __launch_bounds__(256, SV_DS_MINB) k_dstage(double2 *__restrict_
     DS_GRAY(base, a[ix] = r[j]);
   }
 #undef DS_GRAY
+  cp_async_wait_all();
+}
+
+// ----------------------- two-phase tolerance stage passes: eight stage targets per HBM pass
+//
+// k_dstage2: one CTA per 4096-amplitude tile spanning four coalescing low bits L, four
+// targets S1 and four targets S2.  Phase 1 holds, per thread, the 16 elements over S1
+// (thread bits = L and S2) and runs the S1 program; a shared-memory transpose gives each
+// thread the 16 elements over S2 (thread bits = L and S1) for the S2 program; the tile is
+// stored.  Each phase is a k_dstage program (folds, GATE, FLUSH ops) -- a fold group of
+// phase 1 may depend on S2 bits because every phase-1 group is flushed before the
+// transpose.  Eight transform stages per pass instead of four.
+
+constexpr int DS2_MAX = 3 * MS_MAX / 2 + MS_K, DS2_QMAX = 8 * MS_MAX;  // every gate of a phase fits
+
+struct Ds2Params {
+  int32_t nops[2], nbytes, pad;
+  int32_t s1[MS_K], s2[MS_K], lb[MS_K];  // phase-1 slots, phase-2 slots, coalescing low bits
+  int32_t tb[3 * MS_K];                   // all twelve tile bits, ascending
+  double scale;
+  const double2 *tab;
+  uint64_t hdr[2][DS2_MAX];
+  double q[2][DS2_QMAX];
+};
+
+template <int NB>
+__device__ __forceinline__ void ds_exec(double2 (&r)[MS_N], uint64_t base, const uint64_t *hdr, int nops,
+                                        const double *qv, const double2 *tab) {
+  for (int i = 0; i < nops; ++i) {
+    const uint64_t h = hdr[i];
+    const int s = (int)((h >> 2) & 3u);
+    if ((h & 3u) == DS_FLUSH) {
+      const double2 *t = tab + (size_t)((h >> 16) & 0xffu) * 2 * NB * 256;
+      const bool do0 = (h >> 6) & 1u;
+      const double2 f1 = ds_factor<NB>(t, base);
+      const double2 f0 = do0 ? ds_factor<NB>(t + NB * 256, base) : make_double2(1.0, 0.0);
+      switch (s) {
+        case 0: ds_flush<0>(r, f1, f0, do0); break;
+        case 1: ds_flush<1>(r, f1, f0, do0); break;
+        case 2: ds_flush<2>(r, f1, f0, do0); break;
+        default: ds_flush<MS_K - 1>(r, f1, f0, do0); break;
+      }
+      continue;
+    }
+    if (((h >> 4) & 3u) == 2u && !((base >> ((h >> 8) & 63u)) & 1ull)) continue;  // control clear here
+    ds_gate((int)((h >> 16) & 0xffu), r, qv + (h >> 32));
+  }
+}
+
+__device__ __forceinline__ uint64_t spread4(int v, const int32_t (&bits)[MS_K]) {
+  uint64_t x = 0;
+#pragma unroll
+  for (int k = 0; k < MS_K; ++k) x |= (uint64_t)((v >> k) & 1) << bits[k];
+  return x;
+}
+
+#ifndef SV_DS2_MINB
+#define SV_DS2_MINB 2
+#endif
+
+// Persistent; the tile buffer doubles as the prefetch buffer: once phase 2 has its registers,
+// the next tile's phase-1 elements stream into it (cp.async, each thread its own column)
+// while phase 2 computes and stores.
+template <int NB>
+__global__ void __launch_bounds__(256, SV_DS2_MINB) k_dstage2(double2 *__restrict__ a, uint64_t ntiles,
+                                                             const __grid_constant__ Ds2Params P) {
+  extern __shared__ double2 tile[];  // transpose: lo | s1 << 4 | s2 << 8; prefetch: j * 256 + thread
+  const int t = threadIdx.x, lo = t & 15, hi = t >> 4;
+  uint64_t b1[MS_K], b2[MS_K];
+#pragma unroll
+  for (int k = 0; k < MS_K; ++k) b1[k] = 1ull << P.s1[k], b2[k] = 1ull << P.s2[k];
+  const uint64_t lpart = spread4(lo, P.lb);
+  auto cta_base = [&](uint64_t id) {
+    uint64_t cta = id;
+#pragma unroll
+    for (int k = 0; k < 3 * MS_K; ++k) cta = insert_zero(cta, P.tb[k]);
+    return cta;
+  };
+  uint64_t id = blockIdx.x;
+  if (id < ntiles) {
+    const uint64_t base1 = cta_base(id) | lpart | spread4(hi, P.s2);
+#pragma unroll
+    for (int j = 0; j < MS_N; ++j) cp_async16(&tile[j * 256 + t], a + (base1 | ms_off(j, b1)));
+  }
+  cp_async_commit();
+  for (; id < ntiles; id += gridDim.x) {
+    const uint64_t cta = cta_base(id);
+    const uint64_t base1 = cta | lpart | spread4(hi, P.s2);
+    double2 r[MS_N];
+    cp_async_wait_all();
+#pragma unroll
+    for (int j = 0; j < MS_N; ++j) r[j] = tile[j * 256 + t];
+    ds_exec<NB>(r, base1, P.hdr[0], P.nops[0], P.q[0], P.tab);
+    __syncthreads();  // every thread has its prefetched column
+#pragma unroll
+    for (int j = 0; j < MS_N; ++j) tile[lo | (j << 4) | (hi << 8)] = r[j];
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < MS_N; ++j) r[j] = tile[lo | (hi << 4) | (j << 8)];
+    __syncthreads();  // the transpose is read: the buffer takes the next tile
+    const uint64_t nid = id + gridDim.x;
+    if (nid < ntiles) {
+      const uint64_t nb1 = cta_base(nid) | lpart | spread4(hi, P.s2);
+#pragma unroll
+      for (int j = 0; j < MS_N; ++j) cp_async16(&tile[j * 256 + t], a + (nb1 | ms_off(j, b1)));
+    }
+    cp_async_commit();
+    const uint64_t base2 = cta | lpart | spread4(hi, P.s1);
+    ds_exec<NB>(r, base2, P.hdr[1], P.nops[1], P.q[1], P.tab);
+    if (P.scale != 1.0) {
+      const double sc = P.scale;
+#pragma unroll
+      for (int j = 0; j < MS_N; ++j) r[j] = make_double2(r[j].x * sc, r[j].y * sc);
+    }
+#pragma unroll
+    for (int j = 0; j < MS_N; ++j) a[base2 | ms_off(j, b2)] = r[j];
+  }
   cp_async_wait_all();
 }
 
@@ -2210,50 +2329,32 @@ double2 *dtable_slot() {
   return ring[dev] + k * (DT_SLOT_BYTES / sizeof(double2));
 }
 
-// Tolerance-mode stage launch (k_dtable + k_dstage): compile gates[0..n) (targets in <= MS_K
-// bits) into GATE / FLUSH ops and fold groups.
-int run_dstage(double2 *a, int m, const sv_gate *gates, int n, cudaStream_t st) {
-  static thread_local DsParams P;
-  static thread_local DtParams T;
-  if (n < 1 || n > MS_MAX) return fail(SV_EINVAL, "tolerance stage group: %d gates not in [1, %d]", n, MS_MAX);
-  if (m < MS_K) return fail(SV_EINVAL, "tolerance stage group: m=%d below %d", m, MS_K);
-  int bits[MS_K], nb = 0;
-  for (int k = 0; k < n; ++k) {
-    const int t = gates[k].target;
-    bool in = false;
-    for (int s = 0; s < nb; ++s) in |= bits[s] == t;
-    if (in) continue;
-    if (nb == MS_K) return fail(SV_EINVAL, "tolerance stage group: more than %d distinct targets", MS_K);
-    bits[nb++] = t;
-  }
-  // pad with high bits that are no gate's control (a slot control would turn a fold into a
-  // register update), then with any free bit
-  bool ctl[64] = {};
-  for (int k = 0; k < n; ++k)
-    if (gates[k].control >= 0) ctl[gates[k].control] = true;
-  for (int pass = 0; pass < 2; ++pass)
-    for (int b = m - 1; b >= 0 && nb < MS_K; --b) {
-      bool in = false;
-      for (int s = 0; s < nb; ++s) in |= bits[s] == b;
-      if (!in && (pass == 1 || !ctl[b])) bits[nb++] = b;
-    }
-  std::sort(bits, bits + MS_K);
+// Compile one k_dstage program: gates with targets in the four slot bits `bits` (ascending)
+// into GATE / FLUSH ops; fold gates go to T (group ids continue from *ngroups).  Returns
+// SV_OK or an error; capacities are checked.
+struct DsCompiled {
+  int nops = 0, nq = 0;
+  double scale = 1.0;
+};
+
+int compile_ds(const sv_gate *gates, int n, const int (&bits)[MS_K], uint64_t *hdr, int hcap, double *qv,
+               int qcap, DtParams &T, int *ngroups, bool *has0, DsCompiled &out) {
   auto slot = [&](int b) {
     for (int s = 0; s < MS_K; ++s)
       if (bits[s] == b) return s;
     return MS_K;
   };
-  const int nbytes = (m + 7) / 8;
-  int nops = 0, nq = 0, ngroups = 0;
-  double scale = 1.0;
   int open_group[MS_K];
-  bool has0[DS_MAXG] = {};
   for (int s = 0; s < MS_K; ++s) open_group[s] = -1;
-  T.nfold = 0;
+  bool overflow = false;
   auto emit = [&](uint64_t lo, const double *q, int nd) {
-    P.hdr[nops++] = lo | ((uint64_t)nq << 32);
-    if (nd) memcpy(P.q + nq, q, sizeof(double) * nd);
-    nq += nd;
+    if (out.nops >= hcap || out.nq + nd > qcap) {
+      overflow = true;
+      return;
+    }
+    hdr[out.nops++] = lo | ((uint64_t)out.nq << 32);
+    if (nd) memcpy(qv + out.nq, q, sizeof(double) * nd);
+    out.nq += nd;
   };
   auto flush = [&](int s) {
     const int g = open_group[s];
@@ -2264,13 +2365,16 @@ int run_dstage(double2 *a, int m, const sv_gate *gates, int n, cudaStream_t st) 
   for (int k = 0; k < n; ++k) {
     const sv_gate &g = gates[k];
     const int s = slot(g.target), c = g.control, cs = c >= 0 ? slot(c) : MS_K;
+    if (s == MS_K) return fail(SV_EINVAL, "tolerance stage: target %d is not a slot", g.target);
     const int kind = gate_kind(g.q);
     const bool diag = kind == KIND_DIAG || kind == KIND_PHASE;
     if (diag && cs == MS_K) {
       if (open_group[s] < 0) {
-        if (ngroups == DS_MAXG) return fail(SV_EINVAL, "tolerance stage group: more than %d fold groups", DS_MAXG);
-        open_group[s] = ngroups++;
+        if (*ngroups == DS_MAXG) return fail(SV_EINVAL, "tolerance stage: more than %d fold groups", DS_MAXG);
+        if (T.nfold >= DT_MAXF) return fail(SV_EINVAL, "tolerance stage: more than %d folded gates", DT_MAXF);
+        open_group[s] = (*ngroups)++;
       }
+      if (T.nfold >= DT_MAXF) return fail(SV_EINVAL, "tolerance stage: more than %d folded gates", DT_MAXF);
       DtFold &f = T.f[T.nfold++];
       f.group = (int8_t)open_group[s];
       f.c = (int8_t)c;
@@ -2287,27 +2391,156 @@ int run_dstage(double2 *a, int m, const sv_gate *gates, int n, cudaStream_t st) 
     // an uncontrolled Hadamard-like gate: unscaled butterfly, its real factor deferred to one
     // multiply of every amplitude after the pass (it applies to all of them)
     const bool hbf = SV_DS_HBF && kind == KIND_HSHARE && c < 0;
-    if (hbf) scale *= g.q[0];
+    if (hbf) out.scale *= g.q[0];
     const int code = ((hbf ? KIND_HBF : kind) * MS_K + s) * (MS_K + 1) + cs;
     const uint64_t cm = (c >= 0 && cs == MS_K) ? (2ull << 4) | ((uint64_t)(c & 63) << 8) : 0ull;
     emit((uint64_t)DS_GATE | ((uint64_t)s << 2) | cm | ((uint64_t)code << 16), g.q, 8);
   }
   for (int s = 0; s < MS_K; ++s)
     if (open_group[s] >= 0) flush(s);
-  P.nops = nops;
-  P.nbytes = nbytes;
-  for (int s = 0; s < MS_K; ++s) P.bits[s] = bits[s];
-  P.tab = nullptr;
-  if (ngroups) {
-    double2 *tab = dtable_slot();
-    if (!tab) return fail(SV_ECUDA, "tolerance stage group: fold-table buffer allocation failed");
-    T.nbytes = nbytes;
-    T.tab = tab;
-    P.tab = tab;
-    k_dtable<<<ngroups * nbytes * 2, 256, 0, st>>>(T);
-    const int rc = after_launch("k_dtable");
-    if (rc != SV_OK) return rc;
+  if (overflow) return fail(SV_EINVAL, "tolerance stage: program exceeds %d ops / %d gate words", hcap, qcap);
+  return SV_OK;
+}
+
+// Slot bits of a gate run: its distinct targets (at most MS_K), padded with high bits that are
+// neither in `avoid` nor any gate's control, then any free bit; ascending.
+int ds_slots(const sv_gate *gates, int n, int m, uint64_t avoid, int (&bits)[MS_K]) {
+  int nb = 0;
+  for (int k = 0; k < n; ++k) {
+    const int t = gates[k].target;
+    bool in = false;
+    for (int s = 0; s < nb; ++s) in |= bits[s] == t;
+    if (in) continue;
+    if (nb == MS_K) return fail(SV_EINVAL, "tolerance stage: more than %d distinct targets", MS_K);
+    bits[nb++] = t;
   }
+  uint64_t ctl = 0;
+  for (int k = 0; k < n; ++k)
+    if (gates[k].control >= 0) ctl |= 1ull << gates[k].control;
+  for (int pass = 0; pass < 2; ++pass)
+    for (int b = m - 1; b >= 0 && nb < MS_K; --b) {
+      bool in = (avoid >> b) & 1ull;
+      for (int s = 0; s < nb; ++s) in |= bits[s] == b;
+      if (!in && (pass == 1 || !((ctl >> b) & 1ull))) bits[nb++] = b;
+    }
+  if (nb < MS_K) return fail(SV_EINVAL, "tolerance stage: m=%d too small for the slots", m);
+  std::sort(bits, bits + MS_K);
+  return SV_OK;
+}
+
+int launch_dtable(DtParams &T, int ngroups, int nbytes, cudaStream_t st, const double2 **tab_out) {
+  *tab_out = nullptr;
+  if (!ngroups) return SV_OK;
+  double2 *tab = dtable_slot();
+  if (!tab) return fail(SV_ECUDA, "tolerance stage: fold-table buffer allocation failed");
+  T.nbytes = nbytes;
+  T.tab = tab;
+  *tab_out = tab;
+  k_dtable<<<ngroups * nbytes * 2, 256, 0, st>>>(T);
+  return after_launch("k_dtable");
+}
+
+// Two-phase tolerance stage launch (k_dstage2): gates[0..split) target S1, gates[split..n) S2.
+int run_dstage2(double2 *a, int m, const sv_gate *gates, int n, int split, cudaStream_t st) {
+  static thread_local Ds2Params P;
+  static thread_local DtParams T;
+  if (m < 3 * MS_K + 1) return fail(SV_EINVAL, "two-phase stage: m=%d below %d", m, 3 * MS_K + 1);
+  if (split < 1 || split >= n) return fail(SV_EINVAL, "two-phase stage: split %d outside (0, %d)", split, n);
+  int s1[MS_K], s2[MS_K];
+  int rc = ds_slots(gates, split, m, 0, s1);
+  if (rc) return rc;
+  uint64_t used = 0;
+  for (int k = 0; k < MS_K; ++k) used |= 1ull << s1[k];
+  rc = ds_slots(gates + split, n - split, m, used, s2);
+  if (rc) return rc;
+  for (int k = 0; k < MS_K; ++k) used |= 1ull << s2[k];
+  for (int k = 0; k < n; ++k) {  // phase 1 must not touch S2 targets, nor phase 2 S1 targets
+    const bool in1 = (used >> gates[k].target) & 1ull;
+    bool is1 = false;
+    for (int q = 0; q < MS_K; ++q) is1 |= s1[q] == gates[k].target;
+    if (!in1 || (k < split) != is1) return fail(SV_EINVAL, "two-phase stage: gate %d targets the wrong phase", k);
+  }
+  int lb[MS_K], nl = 0;
+  for (int b = 0; b < m && nl < MS_K; ++b)
+    if (!((used >> b) & 1ull)) lb[nl++] = b;
+  if (nl < MS_K) return fail(SV_EINVAL, "two-phase stage: no room for the coalescing bits");
+  T.nfold = 0;
+  int ngroups = 0;
+  bool has0[DS_MAXG] = {};
+  DsCompiled c1, c2;
+  rc = compile_ds(gates, split, s1, P.hdr[0], DS2_MAX, P.q[0], DS2_QMAX, T, &ngroups, has0, c1);
+  if (rc) return rc;
+  rc = compile_ds(gates + split, n - split, s2, P.hdr[1], DS2_MAX, P.q[1], DS2_QMAX, T, &ngroups, has0, c2);
+  if (rc) return rc;
+  const int nbytes = (m + 7) / 8;
+  rc = launch_dtable(T, ngroups, nbytes, st, &P.tab);
+  if (rc) return rc;
+  P.nops[0] = c1.nops;
+  P.nops[1] = c2.nops;
+  P.nbytes = nbytes;
+  P.scale = c1.scale * c2.scale;
+  int tb[3 * MS_K], nt = 0;
+  for (int k = 0; k < MS_K; ++k) {
+    P.s1[k] = s1[k], P.s2[k] = s2[k], P.lb[k] = lb[k];
+    tb[nt++] = s1[k], tb[nt++] = s2[k], tb[nt++] = lb[k];
+  }
+  std::sort(tb, tb + nt);
+  for (int k = 0; k < nt; ++k) P.tb[k] = tb[k];
+  const uint64_t ntiles = 1ull << (m - 3 * MS_K);
+  constexpr int SMEM = 4096 * (int)sizeof(double2);
+  static int per = 0, nsm = 0;
+  if (!per) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(k_dstage2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    cudaFuncSetAttribute(k_dstage2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    cudaFuncSetAttribute(k_dstage2<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    cudaFuncSetAttribute(k_dstage2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    cudaFuncSetAttribute(k_dstage2<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    cudaFuncSetAttribute(k_dstage2<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    cudaFuncSetAttribute(k_dstage2<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    cudaFuncSetAttribute(k_dstage2<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_dstage2<4>, 256, SMEM) != cudaSuccess || per < 1)
+      per = 1;
+  }
+  const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)nsm * per);
+  switch (nbytes) {
+    case 1: k_dstage2<1><<<grid, 256, SMEM, st>>>(a, ntiles, P); break;
+    case 2: k_dstage2<2><<<grid, 256, SMEM, st>>>(a, ntiles, P); break;
+    case 3: k_dstage2<3><<<grid, 256, SMEM, st>>>(a, ntiles, P); break;
+    case 4: k_dstage2<4><<<grid, 256, SMEM, st>>>(a, ntiles, P); break;
+    case 5: k_dstage2<5><<<grid, 256, SMEM, st>>>(a, ntiles, P); break;
+    case 6: k_dstage2<6><<<grid, 256, SMEM, st>>>(a, ntiles, P); break;
+    case 7: k_dstage2<7><<<grid, 256, SMEM, st>>>(a, ntiles, P); break;
+    default: k_dstage2<8><<<grid, 256, SMEM, st>>>(a, ntiles, P); break;
+  }
+  return after_launch("k_dstage2");
+}
+
+// Tolerance-mode stage launch (k_dtable + k_dstage): compile gates[0..n) (targets in <= MS_K
+// bits) into GATE / FLUSH ops and fold groups.
+int run_dstage(double2 *a, int m, const sv_gate *gates, int n, cudaStream_t st) {
+  static thread_local DsParams P;
+  static thread_local DtParams T;
+  if (n < 1 || n > MS_MAX) return fail(SV_EINVAL, "tolerance stage group: %d gates not in [1, %d]", n, MS_MAX);
+  if (m < MS_K) return fail(SV_EINVAL, "tolerance stage group: m=%d below %d", m, MS_K);
+  int bits[MS_K];
+  int rc = ds_slots(gates, n, m, 0, bits);
+  if (rc) return rc;
+  const int nbytes = (m + 7) / 8;
+  int ngroups = 0;
+  bool has0[DS_MAXG] = {};
+  T.nfold = 0;
+  DsCompiled c;
+  rc = compile_ds(gates, n, bits, P.hdr, DS_MAX, P.q, DS_QMAX, T, &ngroups, has0, c);
+  if (rc) return rc;
+  const double scale = c.scale;
+  P.nops = c.nops;
+  P.nbytes = nbytes;
+  for (int k = 0; k < MS_K; ++k) P.bits[k] = bits[k];
+  rc = launch_dtable(T, ngroups, nbytes, st, &P.tab);
+  if (rc) return rc;
   P.nfg = ngroups;
   P.scale = scale;
   P.has0 = 0;
@@ -2477,6 +2710,46 @@ int low_run(int m, const sv_gate *gates, int n, int i) {
   return j - i;
 }
 
+// Tolerance mode: the two-phase stage run from i (k_dstage2): up to MS_K distinct targets, then up
+// to MS_K others, never returning to the first set; per phase at most MS_MAX gates.  Returns its
+// end (i when there is no second phase);
+// *split = the first gate of phase 2.  The same scan recovers the split from a planned group.
+int stage2_run(int m, const sv_gate *gates, int n, int i, int *split) {
+  *split = i;
+  if (m < 3 * MS_K + 2) return i;
+  int S[2][MS_K], ns[2] = {0, 0}, ph = 0, cnt = 0, j = i;
+  auto in = [&](int p, int t) {
+    for (int k = 0; k < ns[p]; ++k)
+      if (S[p][k] == t) return true;
+    return false;
+  };
+  for (; j < n; ++j) {
+    const int t = gates[j].target;
+    if (ph == 0 && !in(0, t)) {
+      if (ns[0] == MS_K) {
+        ph = 1;
+        *split = j;
+        cnt = 0;
+      } else {
+        S[0][ns[0]++] = t;
+      }
+    }
+    if (ph == 1) {
+      if (in(0, t)) break;
+      if (!in(1, t)) {
+        if (ns[1] == MS_K) break;
+        S[1][ns[1]++] = t;
+      }
+    }
+    if (cnt + 1 > MS_MAX) {
+      if (ph == 0) return i;
+      break;
+    }
+    ++cnt;
+  }
+  return ph == 1 ? j : i;
+}
+
 int next_group(int m, const sv_gate *gates, int n, int i, int T, int *kind, bool tol = false) {
   const int L = T - TG_BITS;
   auto tile_cost = [&](int k) {
@@ -2522,6 +2795,21 @@ int next_group(int m, const sv_gate *gates, int n, int i, int T, int *kind, bool
       *kind = SV_GROUP_LOW;
       return i + C;
     }
+    // a two-phase stage run (eight targets) longer than both: one k_dstage2 pass, when it is
+    // mostly diagonal (its folds are what make it cheap; general gates cost the same anywhere)
+    int split;
+    const int e = stage2_run(m, gates, n, i, &split);
+    if (e - i > B && e - i >= A) {
+      int nd = 0;
+      for (int k = i; k < e; ++k) {
+        const int kd = gate_kind(gates[k].q);
+        nd += kd == KIND_DIAG || kd == KIND_PHASE;
+      }
+      if (2 * nd >= e - i) {
+        *kind = SV_GROUP_STAGE2;
+        return e;
+      }
+    }
   }
   if (A <= 1 && B <= 1) {
     *kind = SV_GROUP_GATES;
@@ -2549,6 +2837,12 @@ int exec_group(double2 *a, int m, int T, int kind, const sv_gate *gates, int n, 
   if (kind == SV_GROUP_LOW) {
     if (!tol) return fail(SV_EINVAL, "low-bit groups run in the tolerance mode only (SV_FLAG_TOLERANCE)");
     return run_dlow(a, m, gates, n, st);
+  }
+  if (kind == SV_GROUP_STAGE2) {
+    if (!tol) return fail(SV_EINVAL, "two-phase stage groups run in the tolerance mode only (SV_FLAG_TOLERANCE)");
+    int split;
+    if (stage2_run(m, gates, n, 0, &split) != n) return fail(SV_EINVAL, "not a two-phase stage group");
+    return run_dstage2(a, m, gates, n, split, st);
   }
   if (kind == SV_GROUP_STAGE) {
     if (n == 1) return launch_gate(a, m, gates[0], st);
@@ -2733,7 +3027,7 @@ int sv_apply_group_ex(void *amps, int m, int kind, const sv_gate *gates, int nga
   if (rc != SV_OK) return rc;
   const int tmax = m < SV_FUSED_MAX_TILE ? m : SV_FUSED_MAX_TILE;
   if (tile != 0 && (tile < 9 || tile > tmax)) return fail(SV_EINVAL, "sv_apply_group: tile %d not in [9, %d]", tile, tmax);
-  if (kind < SV_GROUP_GATES || kind > SV_GROUP_LOW) return fail(SV_EINVAL, "sv_apply_group: kind %d", kind);
+  if (kind < SV_GROUP_GATES || kind > SV_GROUP_STAGE2) return fail(SV_EINVAL, "sv_apply_group: kind %d", kind);
   return exec_group((double2 *)amps, m, tile > 0 ? tile : tmax, kind, gates, ngates, (cudaStream_t)stream,
                     flags & SV_FLAG_TOLERANCE);
 }

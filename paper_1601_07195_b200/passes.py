@@ -48,7 +48,7 @@ from .errors import LayoutError, TransportError
 from .kernels import GateMatrix, _as_gate
 
 
-LOCAL_KINDS = ("local_tile", "local_stage", "local_gate", "local_low")
+LOCAL_KINDS = ("local_tile", "local_stage", "local_gate", "local_low", "local_stage2")
 
 
 @dataclass(frozen=True)
@@ -113,7 +113,8 @@ def plan_passes(gates, m: int, tile: int = 0, exact: bool = True) -> list[Pass]:
 
 
 _GROUP_KIND = {_lib.SV_GROUP_GATES: "local_gate", _lib.SV_GROUP_TILE: "local_tile",
-               _lib.SV_GROUP_STAGE: "local_stage", _lib.SV_GROUP_LOW: "local_low"}
+               _lib.SV_GROUP_STAGE: "local_stage", _lib.SV_GROUP_LOW: "local_low",
+               _lib.SV_GROUP_STAGE2: "local_stage2"}
 _KIND_GROUP = {v: k for k, v in _GROUP_KIND.items()}
 
 

@@ -142,3 +142,32 @@ def test_qft28_tolerance_full_size_vs_oracle():
     assert err <= bound(len(circ)), err
     del st, want, host
     torch.cuda.empty_cache()
+
+
+def test_two_phase_stage_groups_mixed_diagonals():
+    """k_dstage2 (eight targets per pass): runs on targets 6..9 then 10..13 with diagonal gates
+    controlled by the other phase's targets (folds that must be flushed at the transpose),
+    by slot bits (register updates), by low and high bits, uncontrolled diagonals with
+    d0 != 1, non-diagonal gates in between (flushes), and controlled Hadamards."""
+    n = 18
+    rng = np.random.default_rng(123)
+    ops = []
+    for phase in ((6, 7, 8, 9), (10, 11, 12, 13)):
+        for t in phase:
+            ops.append(sv.GateOp(sv.hadamard(), t))
+            for _ in range(9):
+                c = int(rng.integers(0, n))
+                if c == t:
+                    continue
+                ph = np.exp(1j * rng.uniform(0, 2 * np.pi))
+                d0 = 1.0 if rng.random() < 0.7 else np.exp(1j * rng.uniform(0, 2 * np.pi))
+                ops.append(sv.GateOp(sv.GateMatrix(np.diag([d0, ph])), t, None if rng.random() < 0.15 else c))
+            if rng.random() < 0.5:
+                c = int(rng.integers(0, n))
+                ops.append(sv.GateOp(sv.random_unitary(rng), t, None if c == t else c))
+    circ = sv.Circuit(n, ops)
+    kinds = [p.kind for p in sv.plan_passes(circ.gates, n, 12, exact=False)]
+    assert "local_stage2" in kinds, kinds
+    v = random_state(rng, n)
+    got, want = run_both(n, circ, v)
+    assert float(np.max(np.abs(got - want))) <= bound(len(circ))

@@ -56,4 +56,7 @@ def test_tolerance_plan_is_order_preserving_cover():
     flat = [op for p in plan for op in p.gates]
     assert len(flat) == len(circ)  # QFT has nothing to merge
     assert all(not p.exact for p in plan)
-    assert [p.kind for p in plan].count("local_stage") == 6
+    # eight transform stages per two-phase pass, the last six stages (qubits 5..0) one low-bit pass
+    assert [p.kind for p in plan] == ["local_stage2"] * 3 + ["local_low"]
+    # the exact planner needs seven passes for the same circuit
+    assert len(sv.plan_passes(circ.gates, 30, 12)) == 7
