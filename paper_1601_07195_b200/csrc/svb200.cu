@@ -21,6 +21,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -178,6 +179,30 @@ __global__ void __launch_bounds__(BLK) k_shfl(double2 *__restrict__ a, uint64_t 
 // gates applied in order on the resident tile (one __syncthreads per gate),
 // one coalesced store.  One HBM read + write of the slice per launch no matter
 // how many gates the run holds.
+
+// First-wave stagger.  CTAs of a uniform-work grid that start together stay in lockstep: every
+// resident CTA of an SM loads, then every one computes, then every one stores, and a pass costs
+// T_HBM + T_FP64.  Offsets between co-resident CTAs persist (a CTA's successor starts when it
+// ends), so delaying the first wave's CTAs by slot * delay (slot = arrival order on the SM)
+// puts the SM's CTAs in different phases for the whole launch.
+__device__ unsigned g_sm_arrivals[1024];
+
+__device__ __forceinline__ void first_wave_stagger(unsigned first_wave, unsigned per_sm, unsigned delay_cycles) {
+  if (delay_cycles == 0u || blockIdx.x >= first_wave) return;
+  __shared__ unsigned s_slot;
+  if (threadIdx.x == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    s_slot = atomicAdd(&g_sm_arrivals[smid & 1023u], 1u) % per_sm;
+  }
+  __syncthreads();
+  const long long wait = (long long)s_slot * delay_cycles;
+  if (wait) {
+    const long long t0 = clock64();
+    while (clock64() - t0 < wait) __nanosleep(128);
+  }
+}
+
 
 struct FusedParams {
   int ngates;
@@ -400,6 +425,7 @@ struct TileSeg {
 struct TileParams {
   int nsegs;
   int last_natural;
+  unsigned first_wave, per_sm, stagger;  // first_wave_stagger (stagger = 0: off)
   int hb[TG_BITS];
   TileSeg seg[TILE_MAX_SEGS];
   TileGate g[TILE_MAX_GATES];
@@ -656,6 +682,7 @@ __global__ void __launch_bounds__(1 << (T - TR), (T <= 12) ? (SV_TILE_THREADS_SM
   for (int k = 0; k < TG_BITS; ++k) hb[k] = P.hb[k];
   const uint64_t tile0 = tile_base<T>(blockIdx.x, hb);  // every non-tile slice bit of this CTA
   const int tid = threadIdx.x;
+  first_wave_stagger(P.first_wave, P.per_sm, P.stagger);
   double2 r[TRN];
   tile_body<T, SPEC>(a, tile0, hb, tid, P, s, r);
   if (SPEC) {
@@ -932,11 +959,59 @@ struct MsParams {
   int32_t hl[2];   // SV_MS_HILANE: slice bits of lane bits 3, 4 (-1: lanes on the low non-slot bits)
   int32_t ins[MS_K + 2];  // zero-insert positions of a group's base, ascending (slots, hl)
   int32_t nins;
+  uint32_t first_wave, per_sm, stagger;  // first_wave_stagger (stagger = 0: off)
 };
+
+// k-th amplitude index j of a thread with bit S set (and bit C set when C is a slot)
+template <int S, int C>
+__host__ __device__ constexpr int ms_hit(int k) {
+  int seen = 0;
+  for (int j = 0; j < MS_N; ++j) {
+    if (!((j >> S) & 1) || (C < MS_K && !((j >> C) & 1))) continue;
+    if (seen++ == k) return j;
+  }
+  return -1;
+}
+
+#ifndef SV_MS_ILP
+// Amplitudes of a phase / diagonal update whose products are formed before any of their fmas.
+// ptxas at the register cap otherwise reuses ONE pair of temporaries for all eight amplitudes
+// (DMUL, DMUL, DFMA, DFMA per amplitude, each DFMA waiting out its DMUL): two FP64 operations in
+// flight per warp, and the pass is bound by FP64 latency instead of FP64 throughput.
+#define SV_MS_ILP 4
+#endif
+
+// r[j] = cmul(qr + i qi, r[j]) for the amplitudes ms_hit<S, C>(0..N-1), SV_MS_ILP at a time
+template <int S, int C>
+__device__ __forceinline__ void ms_scale_hits(double2 (&r)[MS_N], double qr, double qi) {
+  constexpr int N = (C < MS_K) ? MS_N / 4 : MS_N / 2;
+  constexpr int G = SV_MS_ILP < N ? SV_MS_ILP : N;
+#pragma unroll
+  for (int k0 = 0; k0 < N; k0 += G) {
+    double tr[G], ti[G];
+#pragma unroll
+    for (int u = 0; u < G; ++u) {
+      const int j = ms_hit<S, C>(k0 + u);
+      tr[u] = __dmul_rn(r[j].y, qi);
+      ti[u] = __dmul_rn(r[j].x, qi);
+    }
+#pragma unroll
+    for (int u = 0; u < G; ++u) {
+      const int j = ms_hit<S, C>(k0 + u);
+      r[j] = make_double2(__fma_rn(qr, r[j].x, -tr[u]), __fma_rn(qr, r[j].y, ti[u]));
+    }
+  }
+}
 
 // gate on slot S, control slot C (MS_K: none), all pairs of the thread
 template <int S, int C, int KIND>
 __device__ __forceinline__ void ms_apply(double2 (&r)[MS_N], const double *qp) {
+#if SV_MS_ILP > 1
+  if (KIND == KIND_PHASE) {  // a1 = cmul(q[6] + i q[7], a1): the same rounding sequence as spec_pair
+    ms_scale_hits<S, C>(r, qp[6], qp[7]);
+    return;
+  }
+#endif
   double q[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) q[i] = qp[i];
@@ -1138,7 +1213,10 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
-__global__ void __launch_bounds__(MS_BLK, SV_MS_MINB * 256 / MS_BLK) k_mstage(double2 *__restrict__ a,
+#ifndef SV_MS_THREADS
+#define SV_MS_THREADS (SV_MS_MINB * 256)  // resident threads per SM the register budget must allow
+#endif
+__global__ void __launch_bounds__(MS_BLK, SV_MS_THREADS / MS_BLK) k_mstage(double2 *__restrict__ a,
                                                                           uint64_t ngroups,
                                                                           const __grid_constant__ MsParams P) {
   const uint64_t p = (uint64_t)blockIdx.x * MS_BLK + threadIdx.x;
@@ -1159,6 +1237,7 @@ __global__ void __launch_bounds__(MS_BLK, SV_MS_MINB * 256 / MS_BLK) k_mstage(do
     for (int s = 0; s < MS_K; ++s) base = insert_zero(base, P.bits[s]);
   }
   const bool live = p < ngroups;
+  first_wave_stagger(P.first_wave, P.per_sm, P.stagger);
   double2 r[MS_N];
 #pragma unroll
   for (int j = 0; j < MS_N; ++j) r[j] = live ? a[base | ms_off(j, b)] : make_double2(1.0, 1.0);
@@ -1434,11 +1513,11 @@ __device__ __forceinline__ uint64_t spread4(int v, const int32_t (&bits)[MS_K]) 
 
 // Persistent; the tile buffer doubles as the prefetch buffer: once phase 2 has its registers,
 // the next tile's phase-1 elements stream into it (cp.async, each thread its own column)
-// while phase 2 computes and stores.
-template <int NB>
-__global__ void __launch_bounds__(256, SV_DS2_MINB) k_dstage2(double2 *__restrict__ a, uint64_t ntiles,
-                                                             const __grid_constant__ Ds2Params P) {
-  extern __shared__ double2 tile[];  // transpose: lo | s1 << 4 | s2 << 8; prefetch: j * 256 + thread
+// while phase 2 computes and stores.  PT carries the tile geometry (s1, s2, lb, tb, scale);
+// F1 / F2 run the two phases on a thread's 16 registers.
+template <class PT, class F1, class F2>
+__device__ __forceinline__ void ds2_tiles(double2 *__restrict__ a, uint64_t ntiles, const PT &P, double2 *tile,
+                                          F1 phase1, F2 phase2) {
   const int t = threadIdx.x, lo = t & 15, hi = t >> 4;
   uint64_t b1[MS_K], b2[MS_K];
 #pragma unroll
@@ -1464,7 +1543,7 @@ __global__ void __launch_bounds__(256, SV_DS2_MINB) k_dstage2(double2 *__restric
     cp_async_wait_all();
 #pragma unroll
     for (int j = 0; j < MS_N; ++j) r[j] = tile[j * 256 + t];
-    ds_exec<NB>(r, base1, P.hdr[0], P.nops[0], P.q[0], P.tab);
+    phase1(r, base1);
     __syncthreads();  // every thread has its prefetched column
 #pragma unroll
     for (int j = 0; j < MS_N; ++j) tile[lo | (j << 4) | (hi << 8)] = r[j];
@@ -1480,7 +1559,7 @@ __global__ void __launch_bounds__(256, SV_DS2_MINB) k_dstage2(double2 *__restric
     }
     cp_async_commit();
     const uint64_t base2 = cta | lpart | spread4(hi, P.s1);
-    ds_exec<NB>(r, base2, P.hdr[1], P.nops[1], P.q[1], P.tab);
+    phase2(r, base2);
     if (P.scale != 1.0) {
       const double sc = P.scale;
 #pragma unroll
@@ -1490,6 +1569,133 @@ __global__ void __launch_bounds__(256, SV_DS2_MINB) k_dstage2(double2 *__restric
     for (int j = 0; j < MS_N; ++j) a[base2 | ms_off(j, b2)] = r[j];
   }
   cp_async_wait_all();
+}
+
+template <int NB>
+__global__ void __launch_bounds__(256, SV_DS2_MINB) k_dstage2(double2 *__restrict__ a, uint64_t ntiles,
+                                                             const __grid_constant__ Ds2Params P) {
+  extern __shared__ double2 tile[];  // transpose: lo | s1 << 4 | s2 << 8; prefetch: j * 256 + thread
+  ds2_tiles(
+      a, ntiles, P, tile,
+      [&](double2(&r)[MS_N], uint64_t base) { ds_exec<NB>(r, base, P.hdr[0], P.nops[0], P.q[0], P.tab); },
+      [&](double2(&r)[MS_N], uint64_t base) { ds_exec<NB>(r, base, P.hdr[1], P.nops[1], P.q[1], P.tab); });
+}
+
+// ---------------------------------------------- compiled transform phases (tolerance mode)
+//
+// The op interpreter above pays a header load, a decode and a branch tree per op -- about as
+// many issue slots as the FP64 work of a transform pass, and long dependent latencies with 16
+// warps per SM.  A phase whose gate list has the shape of transform stages,
+//   forward:  for slots s descending   [butterfly on s]  then  phases on s (controls: lower slots or non-slots)
+//   inverse:  for slots s ascending    phases on s (same controls)  then  [butterfly on s]
+// (the stages of the reference's build_qft / its inverse, circuits.py:141-156) runs as straight-line
+// code instead: per slot one butterfly over the 8 pairs and ONE complex factor per amplitude with
+// the slot bit set -- fold-table product (controls outside the slots) times the host-multiplied
+// product of the in-slot phases, indexed by the amplitude's lower slot bits.
+struct XfPhase {
+  int32_t hmask;  // bit s: slot s has its Hadamard-like butterfly
+  int32_t fmask;  // bit s: slot s has a fold group, group[s]
+  int32_t pmask;  // bit s: slot s has in-slot controlled phases, phw[s][1 .. 2^s - 1]
+  int32_t pad;
+  int32_t group[MS_K];
+  double2 phw[MS_K][MS_N / 2];  // phw[s][k]: product of slot s's phases whose control slots are the set bits of k
+};
+
+struct Xf2Params {
+  int32_t nbytes, pad;
+  int32_t s1[MS_K], s2[MS_K], lb[MS_K];
+  int32_t tb[3 * MS_K];
+  double scale;
+  const double2 *tab;
+  XfPhase ph[2];
+};
+
+template <int S>
+__device__ __forceinline__ void xf_bfly(double2 (&r)[MS_N]) {
+#pragma unroll
+  for (int j = 0; j < MS_N; ++j) {
+    if ((j >> S) & 1) continue;
+    spec_pair<KIND_HBF>(r[j], r[j | (1 << S)], nullptr);
+  }
+}
+
+// r[j] *= f * phw[S][j's lower slot bits] for every j with bit S set
+template <int S>
+__device__ __forceinline__ void xf_diag(double2 (&r)[MS_N], const XfPhase &X, double2 f) {
+  constexpr int NK = 1 << S;
+  const bool hasf = (X.fmask >> S) & 1, hasp = (X.pmask >> S) & 1;
+  if (!hasp) {
+    if (!hasf) return;
+#pragma unroll
+    for (int j = 0; j < MS_N; ++j)
+      if ((j >> S) & 1) r[j] = cmul2(f, r[j]);
+    return;
+  }
+  double2 w[NK];
+  w[0] = f;
+#pragma unroll
+  for (int k = 1; k < NK; ++k) w[k] = hasf ? cmul2(f, X.phw[S][k]) : X.phw[S][k];
+#pragma unroll
+  for (int j = 0; j < MS_N; ++j) {
+    if (!((j >> S) & 1)) continue;
+    const int k = j & (NK - 1);
+    if (k == 0) {
+      if (hasf) r[j] = cmul2(w[0], r[j]);
+    } else {
+      r[j] = cmul2(w[k], r[j]);
+    }
+  }
+}
+
+template <int S, bool INV>
+__device__ __forceinline__ void xf_slot(double2 (&r)[MS_N], const XfPhase &X, double2 f) {
+  if (INV) xf_diag<S>(r, X, f);
+  if ((X.hmask >> S) & 1) xf_bfly<S>(r);
+  if (!INV) xf_diag<S>(r, X, f);
+}
+
+template <int NB, bool INV>
+__device__ __forceinline__ void xf_exec(double2 (&r)[MS_N], uint64_t base, const XfPhase &X,
+                                        const double2 *__restrict__ tab) {
+  static_assert(MS_K == 4, "compiled transform phases assume four slots");
+  // the fold factors of all four slots first: their table loads are in flight together
+  double2 e[MS_K][NB];
+#pragma unroll
+  for (int s = 0; s < MS_K; ++s) {
+    const bool hasf = (X.fmask >> s) & 1;
+    const double2 *t = tab + (size_t)(hasf ? X.group[s] : 0) * 2 * NB * 256;
+#pragma unroll
+    for (int k = 0; k < NB; ++k) e[s][k] = hasf ? t[k * 256 + ((base >> (8 * k)) & 255u)] : make_double2(1.0, 0.0);
+  }
+  double2 f[MS_K];
+#pragma unroll
+  for (int s = 0; s < MS_K; ++s) {
+    f[s] = e[s][0];
+    if ((X.fmask >> s) & 1) {
+#pragma unroll
+      for (int k = 1; k < NB; ++k) f[s] = cmul2(e[s][k], f[s]);
+    }
+  }
+  if (!INV) {
+    xf_slot<3, false>(r, X, f[3]);
+    xf_slot<2, false>(r, X, f[2]);
+    xf_slot<1, false>(r, X, f[1]);
+    xf_slot<0, false>(r, X, f[0]);
+  } else {
+    xf_slot<0, true>(r, X, f[0]);
+    xf_slot<1, true>(r, X, f[1]);
+    xf_slot<2, true>(r, X, f[2]);
+    xf_slot<3, true>(r, X, f[3]);
+  }
+}
+
+template <int NB, bool INV>
+__global__ void __launch_bounds__(256, SV_DS2_MINB) k_xstage2(double2 *__restrict__ a, uint64_t ntiles,
+                                                             const __grid_constant__ Xf2Params P) {
+  extern __shared__ double2 tile[];
+  ds2_tiles(
+      a, ntiles, P, tile, [&](double2(&r)[MS_N], uint64_t base) { xf_exec<NB, INV>(r, base, P.ph[0], P.tab); },
+      [&](double2(&r)[MS_N], uint64_t base) { xf_exec<NB, INV>(r, base, P.ph[1], P.tab); });
 }
 
 // ------------------------------ tolerance-mode low-bit passes (targets in slice bits 0..5)
@@ -2141,13 +2347,36 @@ int plan_tile(const sv_gate *gates, int n, int T, const int (&hb)[TG_BITS], Tile
   return gi;
 }
 
+// Resident CTAs per SM of a kernel times the SM count (the first wave), cached per kernel.
+template <typename K>
+void wave_shape(K kern, int threads, size_t smem, unsigned &first_wave, unsigned &per_sm) {
+  int dev = 0, nsm = 0, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, threads, smem) != cudaSuccess || per < 1) per = 1;
+  per_sm = (unsigned)per;
+  first_wave = (unsigned)(nsm * per);
+}
+
+int env_int(const char *name, int dflt) {
+  const char *v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
+}
+
 template <int T, bool SPEC>
-int launch_tile_ts(double2 *a, int m, const TileParams &P, cudaStream_t st) {
+int launch_tile_ts(double2 *a, int m, const TileParams &P0, cudaStream_t st) {
   const size_t smem = sizeof(double2) << T;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k_tile<T, SPEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return fail(SV_ECUDA, "tile: smem attribute: %s", cudaGetErrorString(e));
   }
+  static unsigned fw = 0, per = 0;
+  if (!fw) wave_shape(k_tile<T, SPEC>, 1 << (T - TR), smem, fw, per);
+  static const int stagger = env_int("SVB_TILE_STAGGER", 0);
+  TileParams &P = const_cast<TileParams &>(P0);
+  P.first_wave = fw;
+  P.per_sm = per;
+  P.stagger = (1ull << (m - T)) > 2ull * fw ? (unsigned)stagger : 0u;
   k_tile<T, SPEC><<<(unsigned)(1ull << (m - T)), 1 << (T - TR), smem, st>>>(a, P);
   return after_launch("k_tile");
 }
@@ -2301,6 +2530,12 @@ int run_mstage(double2 *a, int m, const sv_gate *gates, int n, cudaStream_t st) 
     R.range = (R.hi == 31 ? 0xffffffffu : ((2u << R.hi) - 1u)) & ~((1u << R.lo) - 1u);
   }
   const uint64_t ng = 1ull << (m - MS_K);
+  static unsigned fw = 0, per = 0;
+  if (!fw) wave_shape(k_mstage, MS_BLK, 0, fw, per);
+  static const int stagger = env_int("SVB_MS_STAGGER", 0);
+  P.first_wave = fw;
+  P.per_sm = per;
+  P.stagger = grid_for(ng, MS_BLK) > 2 * fw ? (unsigned)stagger : 0u;
   k_mstage<<<grid_for(ng, MS_BLK), MS_BLK, 0, st>>>(a, ng, P);
   return after_launch("k_mstage");
 }
@@ -2440,6 +2675,124 @@ int launch_dtable(DtParams &T, int ngroups, int nbytes, cudaStream_t st, const d
   return after_launch("k_dtable");
 }
 
+// Does the gate run have the shape of transform stages over the slots `bits` (see XfPhase)?
+// Blocks in strictly descending (forward) or ascending (inverse) slot order; a block is the
+// slot's uncontrolled Hadamard-like gate (at most one; first in a forward block, last in an
+// inverse one) and phase gates diag(1, e) on the slot controlled by a lower slot, a non-slot
+// bit or nothing.  On a match fills X, appends the fold gates to T (groups continue from
+// *ngroups) and multiplies *scale by the butterflies' factors.
+bool match_xform(const sv_gate *gates, int n, const int (&bits)[MS_K], bool inverse, XfPhase &X, DtParams &T,
+                 int *ngroups, double *scale) {
+  auto slot = [&](int b) {
+    for (int s = 0; s < MS_K; ++s)
+      if (bits[s] == b) return s;
+    return MS_K;
+  };
+  // pass 1: validate, count what would be appended
+  int cur = -1, nfold = 0, ngrp = 0;
+  bool closed = false, seen[MS_K] = {}, hasfold[MS_K] = {};
+  for (int k = 0; k < n; ++k) {
+    const sv_gate &g = gates[k];
+    const int s = slot(g.target), kind = gate_kind(g.q);
+    if (s == MS_K) return false;
+    if (s != cur) {  // a new block
+      if (seen[s]) return false;
+      if (cur >= 0 && (inverse ? s < cur : s > cur)) return false;
+      seen[s] = true;
+      cur = s;
+      closed = false;
+    }
+    if (kind == KIND_HSHARE && g.control < 0) {
+      if (closed) return false;
+      if (!inverse) {
+        // forward: the butterfly opens its block
+        if (k > 0 && slot(gates[k - 1].target) == s) return false;
+      } else {
+        closed = true;  // inverse: nothing of this slot may follow
+      }
+      continue;
+    }
+    if (kind != KIND_PHASE || closed) return false;
+    const int cs = g.control >= 0 ? slot(g.control) : MS_K;
+    if (cs < MS_K) {
+      if (cs >= s) return false;
+    } else {
+      if (!hasfold[s]) ++ngrp;
+      hasfold[s] = true;
+      ++nfold;
+    }
+  }
+  if (*ngroups + ngrp > DS_MAXG || T.nfold + nfold > DT_MAXF) return false;
+  // pass 2: fill
+  memset(&X, 0, sizeof(X));
+  for (int s = 0; s < MS_K; ++s)
+    for (int k = 0; k < MS_N / 2; ++k) X.phw[s][k] = make_double2(1.0, 0.0);
+  for (int k = 0; k < n; ++k) {
+    const sv_gate &g = gates[k];
+    const int s = slot(g.target), kind = gate_kind(g.q);
+    if (kind == KIND_HSHARE && g.control < 0) {
+      X.hmask |= 1 << s;
+      *scale *= g.q[0];
+      continue;
+    }
+    const int cs = g.control >= 0 ? slot(g.control) : MS_K;
+    if (cs < MS_K) {
+      X.pmask |= 1 << s;
+      for (int j = 0; j < (1 << s); ++j) {
+        if (!((j >> cs) & 1)) continue;
+        const double2 w = X.phw[s][j];
+        X.phw[s][j] = make_double2(w.x * g.q[6] - w.y * g.q[7], w.x * g.q[7] + w.y * g.q[6]);
+      }
+    } else {
+      if (!((X.fmask >> s) & 1)) {
+        X.fmask |= 1 << s;
+        X.group[s] = (*ngroups)++;
+      }
+      DtFold &f = T.f[T.nfold++];
+      f.group = (int8_t)X.group[s];
+      f.c = (int8_t)g.control;
+      f.pad = 0;
+      f.pad2 = 0;
+      f.d[0] = 1.0;
+      f.d[1] = 0.0;
+      f.d[2] = g.q[6];
+      f.d[3] = g.q[7];
+    }
+  }
+  return true;
+}
+
+#ifndef SV_XFORM
+#define SV_XFORM 1  // compiled transform phases (k_xstage2) when both phases of a two-phase pass match
+#endif
+
+template <int NB, bool INV>
+void launch_xstage2_t(double2 *a, uint64_t ntiles, const Xf2Params &X, cudaStream_t st) {
+  constexpr int SMEM = 4096 * (int)sizeof(double2);
+  static int per = 0, nsm = 0;
+  if (!per) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(k_xstage2<NB, INV>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_xstage2<NB, INV>, 256, SMEM) != cudaSuccess || per < 1)
+      per = 1;
+  }
+  const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)nsm * per);
+  k_xstage2<NB, INV><<<grid, 256, SMEM, st>>>(a, ntiles, X);
+}
+
+template <bool INV>
+bool launch_xstage2(double2 *a, uint64_t ntiles, const Xf2Params &X, cudaStream_t st) {
+  switch (X.nbytes) {
+    case 2: launch_xstage2_t<2, INV>(a, ntiles, X, st); return true;
+    case 3: launch_xstage2_t<3, INV>(a, ntiles, X, st); return true;
+    case 4: launch_xstage2_t<4, INV>(a, ntiles, X, st); return true;
+    case 5: launch_xstage2_t<5, INV>(a, ntiles, X, st); return true;
+    default: return false;
+  }
+}
+
 // Two-phase tolerance stage launch (k_dstage2): gates[0..split) target S1, gates[split..n) S2.
 int run_dstage2(double2 *a, int m, const sv_gate *gates, int n, int split, cudaStream_t st) {
   static thread_local Ds2Params P;
@@ -2464,6 +2817,34 @@ int run_dstage2(double2 *a, int m, const sv_gate *gates, int n, int split, cudaS
   for (int b = 0; b < m && nl < MS_K; ++b)
     if (!((used >> b) & 1ull)) lb[nl++] = b;
   if (nl < MS_K) return fail(SV_EINVAL, "two-phase stage: no room for the coalescing bits");
+  const int nbytes = (m + 7) / 8;
+  const uint64_t ntiles = 1ull << (m - 3 * MS_K);
+#if SV_XFORM
+  if (nbytes >= 2 && nbytes <= 5) {  // both phases shaped like transform stages: the compiled kernel
+    static thread_local Xf2Params X;
+    for (int inverse = 0; inverse < 2; ++inverse) {
+      T.nfold = 0;
+      int ng = 0;
+      double scale = 1.0;
+      if (!match_xform(gates, split, s1, inverse != 0, X.ph[0], T, &ng, &scale) ||
+          !match_xform(gates + split, n - split, s2, inverse != 0, X.ph[1], T, &ng, &scale))
+        continue;
+      rc = launch_dtable(T, ng, nbytes, st, &X.tab);
+      if (rc) return rc;
+      X.nbytes = nbytes;
+      X.scale = scale;
+      int xt[3 * MS_K], nx = 0;
+      for (int k = 0; k < MS_K; ++k) {
+        X.s1[k] = s1[k], X.s2[k] = s2[k], X.lb[k] = lb[k];
+        xt[nx++] = s1[k], xt[nx++] = s2[k], xt[nx++] = lb[k];
+      }
+      std::sort(xt, xt + nx);
+      for (int k = 0; k < nx; ++k) X.tb[k] = xt[k];
+      if (inverse ? launch_xstage2<true>(a, ntiles, X, st) : launch_xstage2<false>(a, ntiles, X, st))
+        return after_launch("k_xstage2");
+    }
+  }
+#endif
   T.nfold = 0;
   int ngroups = 0;
   bool has0[DS_MAXG] = {};
@@ -2472,7 +2853,6 @@ int run_dstage2(double2 *a, int m, const sv_gate *gates, int n, int split, cudaS
   if (rc) return rc;
   rc = compile_ds(gates + split, n - split, s2, P.hdr[1], DS2_MAX, P.q[1], DS2_QMAX, T, &ngroups, has0, c2);
   if (rc) return rc;
-  const int nbytes = (m + 7) / 8;
   rc = launch_dtable(T, ngroups, nbytes, st, &P.tab);
   if (rc) return rc;
   P.nops[0] = c1.nops;
@@ -2486,7 +2866,6 @@ int run_dstage2(double2 *a, int m, const sv_gate *gates, int n, int split, cudaS
   }
   std::sort(tb, tb + nt);
   for (int k = 0; k < nt; ++k) P.tb[k] = tb[k];
-  const uint64_t ntiles = 1ull << (m - 3 * MS_K);
   constexpr int SMEM = 4096 * (int)sizeof(double2);
   static int per = 0, nsm = 0;
   if (!per) {

@@ -1,0 +1,16 @@
+mkdir -p gpurun_out
+OUT=gpurun_out
+T=/tmp/ncu_caps; mkdir -p $T
+python tools/profile_kernels.py 28 qft_tol > $OUT/tol_plain.log 2>&1; tail -1 $OUT/tol_plain.log
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_tol.csv python tools/profile_kernels.py 28 qft_tol > /dev/null 2>&1
+grep -c k_d $OUT/launches_tol.csv
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_dstage2 -s 3 -c 1 -f -o $T/prof_dstage2 \
+    python tools/profile_kernels.py 28 qft_tol > $OUT/ncu_dstage2.log 2>&1; tail -1 $OUT/ncu_dstage2.log
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_dlow -s 1 -c 1 -f -o $T/prof_dlow \
+    python tools/profile_kernels.py 28 qft_tol > $OUT/ncu_dlow.log 2>&1; tail -1 $OUT/ncu_dlow.log
+for k in prof_dstage2 prof_dlow; do
+  ncu -i $T/$k.ncu-rep --page raw --csv > $OUT/$k.raw.csv 2>/dev/null
+  ncu -i $T/$k.ncu-rep --page source --csv --print-source sass > $OUT/$k.sass.csv 2>/dev/null
+  gzip -f $OUT/$k.sass.csv
+done
+ls -la $OUT | tail -8

@@ -35,6 +35,8 @@ for _ in range(2):
         sv.run_circuit(st, qft, fusion=fc)
     if what in ("all", "random"):
         sv.run_circuit(st, rand, fusion=fc)
+    if what == "qft_tol":  # tolerance planner: k_dstage2 passes, then k_dlow
+        sv.run_circuit(st, qft, fusion=sv.FusionConfig(l_c=12, passes=True, exact=False))
 torch.cuda.synchronize()
 plan = sv.plan_passes(rand.gates, n, 12)
 print("ok; random plan:", [(p.kind, len(p.gates)) for p in plan])
