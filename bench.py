@@ -661,6 +661,7 @@ def run_ours(args, world, rank, local):
     secondary = {}
     if not args.no_secondary and args.n is None:
         plan = [("controlled", "controlled", "none"), ("random_passes", "random", "passes"),
+                ("random_tolerance", "random", "tolerance"),
                 ("qft_passes", "qft", "passes"), ("qft_tolerance", "qft", "tolerance")]
         for name, wl, fz in plan:
             if wl == args.workload and fz == fusion:

@@ -123,6 +123,16 @@ int sv_plan_gates_ex(int m, const sv_gate *gates, int ngates, int tile, int flag
 int sv_apply_group_ex(void *amps, int m, int kind, const sv_gate *gates, int ngates, int tile, int flags,
                       void *stream);
 
+/* How a two-phase tolerance group (SV_GROUP_STAGE2) will run -- pure host code, no GPU:
+ * SV_SHAPE_INTERPRETED (the op interpreter of k_dstage2), SV_SHAPE_FORWARD / SV_SHAPE_INVERSE
+ * (both phases have the shape of transform stages, the reference's build_qft stages
+ * circuits.py:141-156 or their inverse: straight-line compiled phases, k_xstage2), or a
+ * negative error when the gates are not a two-phase group.  No reference counterpart. */
+#define SV_SHAPE_INTERPRETED 0
+#define SV_SHAPE_FORWARD 1
+#define SV_SHAPE_INVERSE 2
+int sv_stage2_shape(int m, const sv_gate *gates, int ngates);
+
 /* Staged variant of sv_exchange for the NCCL data plane (NvlinkFabric(data_plane=
  * "nccl"), the reference's chunked pipeline distributed.py:205-290 over NCCL
  * send/recv): `buf` holds the partner's elements j0 .. j0+count_j-1 of this rank's

@@ -24,6 +24,7 @@ SV_MSTAGE_MAX_GATES, SV_MSTAGE_MAX_TARGETS = 128, 4
 SV_TILE_GATHER = 8
 SV_GROUP_GATES, SV_GROUP_TILE, SV_GROUP_STAGE, SV_GROUP_LOW, SV_GROUP_STAGE2 = 0, 1, 2, 3, 4
 SV_FLAG_TOLERANCE = 1
+SV_SHAPE_INTERPRETED, SV_SHAPE_FORWARD, SV_SHAPE_INVERSE = 0, 1, 2
 ABI_VERSION = 1
 
 EXPORTS = (
@@ -32,7 +33,7 @@ EXPORTS = (
     "sv_exchange_stage", "sv_norm_sq", "sv_init_random", "sv_scale", "sv_init_basis",
     "sv_copy", "sv_ipc_handle", "sv_ipc_open", "sv_ipc_close", "sv_diag_global", "sv_diag_fix",
     "sv_swap_global", "sv_max_abs_diff", "sv_apply_gates_ex", "sv_plan_gates_ex", "sv_apply_group_ex",
-    "sv_pair_update",
+    "sv_pair_update", "sv_stage2_shape",
 )
 
 
@@ -77,6 +78,7 @@ def load() -> ctypes.CDLL:
         "sv_plan_gates_ex": ([i, ctypes.POINTER(SvGate), i, i, i, ctypes.POINTER(ctypes.c_int32),
                               ctypes.POINTER(ctypes.c_int32), i], i),
         "sv_apply_group_ex": ([vp, i, i, ctypes.POINTER(SvGate), i, i, i, vp], i),
+        "sv_stage2_shape": ([i, ctypes.POINTER(SvGate), i], i),
         "sv_exchange": ([vp, vp, i, i, i, dp, vp], i),
         "sv_exchange_chunk": ([vp, vp, i, i, i, dp, u64, u64, vp], i),
         "sv_pair_update": ([vp, vp, u64, i, dp, vp], i),

@@ -2904,13 +2904,10 @@ bool launch_xstage2(double2 *a, uint64_t ntiles, const Xf2Params &X, cudaStream_
 #undef XS2_CASE
 }
 
-// Two-phase tolerance stage launch (k_dstage2): gates[0..split) target S1, gates[split..n) S2.
-int run_dstage2(double2 *a, int m, const sv_gate *gates, int n, int split, cudaStream_t st) {
-  static thread_local Ds2Params P;
-  static thread_local DtParams T;
+// The slot sets of a two-phase group (gates[0..split) on S1, the rest on S2) and its coalescing bits.
+int stage2_slots(int m, const sv_gate *gates, int n, int split, int (&s1)[MS_K], int (&s2)[MS_K], int (&lb)[MS_K]) {
   if (m < 3 * MS_K + 1) return fail(SV_EINVAL, "two-phase stage: m=%d below %d", m, 3 * MS_K + 1);
   if (split < 1 || split >= n) return fail(SV_EINVAL, "two-phase stage: split %d outside (0, %d)", split, n);
-  int s1[MS_K], s2[MS_K];
   int rc = ds_slots(gates, split, m, 0, s1);
   if (rc) return rc;
   uint64_t used = 0;
@@ -2924,22 +2921,46 @@ int run_dstage2(double2 *a, int m, const sv_gate *gates, int n, int split, cudaS
     for (int q = 0; q < MS_K; ++q) is1 |= s1[q] == gates[k].target;
     if (!in1 || (k < split) != is1) return fail(SV_EINVAL, "two-phase stage: gate %d targets the wrong phase", k);
   }
-  int lb[MS_K], nl = 0;
+  int nl = 0;
   for (int b = 0; b < m && nl < MS_K; ++b)
     if (!((used >> b) & 1ull)) lb[nl++] = b;
   if (nl < MS_K) return fail(SV_EINVAL, "two-phase stage: no room for the coalescing bits");
+  return SV_OK;
+}
+
+// 0: the interpreter; 1 / 2: both phases compile as forward / inverse transform stages (fills X, T).
+int stage2_shape(int m, const sv_gate *gates, int n, int split, const int (&s1)[MS_K], const int (&s2)[MS_K],
+                 Xf2Params &X, DtParams &T, int *ngroups, double *scale) {
+#if SV_XFORM
+  const int nbytes = (m + 7) / 8;
+  if (nbytes < 2 || nbytes > 5) return 0;
+  for (int inverse = 0; inverse < 2; ++inverse) {
+    T.nfold = 0;
+    *ngroups = 0;
+    *scale = 1.0;
+    if (match_xform(gates, split, s1, inverse != 0, X.ph[0], T, ngroups, scale) &&
+        match_xform(gates + split, n - split, s2, inverse != 0, X.ph[1], T, ngroups, scale))
+      return 1 + inverse;
+  }
+#endif
+  return 0;
+}
+
+// Two-phase tolerance stage launch (k_dstage2): gates[0..split) target S1, gates[split..n) S2.
+int run_dstage2(double2 *a, int m, const sv_gate *gates, int n, int split, cudaStream_t st) {
+  static thread_local Ds2Params P;
+  static thread_local DtParams T;
+  int s1[MS_K], s2[MS_K], lb[MS_K];
+  int rc = stage2_slots(m, gates, n, split, s1, s2, lb);
+  if (rc) return rc;
   const int nbytes = (m + 7) / 8;
   const uint64_t ntiles = 1ull << (m - 3 * MS_K);
-#if SV_XFORM
-  if (nbytes >= 2 && nbytes <= 5) {  // both phases shaped like transform stages: the compiled kernel
+  {  // both phases shaped like transform stages: the compiled kernel
     static thread_local Xf2Params X;
-    for (int inverse = 0; inverse < 2; ++inverse) {
-      T.nfold = 0;
-      int ng = 0;
-      double scale = 1.0;
-      if (!match_xform(gates, split, s1, inverse != 0, X.ph[0], T, &ng, &scale) ||
-          !match_xform(gates + split, n - split, s2, inverse != 0, X.ph[1], T, &ng, &scale))
-        continue;
+    int ng = 0;
+    double scale = 1.0;
+    const int shape = stage2_shape(m, gates, n, split, s1, s2, X, T, &ng, &scale);
+    if (shape) {
       rc = launch_dtable(T, ng, nbytes, st, &X.tab);
       if (rc) return rc;
       X.nbytes = nbytes;
@@ -2951,11 +2972,10 @@ int run_dstage2(double2 *a, int m, const sv_gate *gates, int n, int split, cudaS
       }
       std::sort(xt, xt + nx);
       for (int k = 0; k < nx; ++k) X.tb[k] = xt[k];
-      if (inverse ? launch_xstage2<true>(a, ntiles, X, st) : launch_xstage2<false>(a, ntiles, X, st))
+      if (shape == 2 ? launch_xstage2<true>(a, ntiles, X, st) : launch_xstage2<false>(a, ntiles, X, st))
         return after_launch("k_xstage2");
     }
   }
-#endif
   T.nfold = 0;
   int ngroups = 0;
   bool has0[DS_MAXG] = {};
@@ -3558,6 +3578,23 @@ int sv_plan_gates_ex(int m, const sv_gate *gates, int ngates, int tile, int flag
     ++ng;
   }
   return ng;
+}
+
+int sv_stage2_shape(int m, const sv_gate *gates, int ngates) {
+  if (!gates) return fail(SV_EINVAL, "sv_stage2_shape: null pointer");
+  if (m < 1 || m > 62 || ngates < 2) return fail(SV_EINVAL, "sv_stage2_shape: m=%d / ngates=%d invalid", m, ngates);
+  int rc = check_gates("sv_stage2_shape", m, gates, ngates, m);
+  if (rc != SV_OK) return rc;
+  int split;
+  if (stage2_run(m, gates, ngates, 0, &split) != ngates) return fail(SV_EINVAL, "sv_stage2_shape: not a two-phase stage group");
+  int s1[MS_K], s2[MS_K], lb[MS_K];
+  rc = stage2_slots(m, gates, ngates, split, s1, s2, lb);
+  if (rc) return rc;
+  static thread_local Xf2Params X;
+  static thread_local DtParams T;
+  int ng = 0;
+  double scale = 1.0;
+  return stage2_shape(m, gates, ngates, split, s1, s2, X, T, &ng, &scale);
 }
 
 int sv_plan_gates(int m, const sv_gate *gates, int ngates, int tile, int32_t *group_end, int32_t *group_kind,

@@ -356,3 +356,39 @@ def test_m33_qft_passes_vs_closed_form(big33):
     sv.run_circuit(st, circ)
     assert checksum(big33.a) == h_pass, "pass-fused transform differs from per-gate at n = 33"
     big33.reset()
+
+
+def test_m33_qft_tolerance_vs_closed_form(big33):
+    """The tolerance-mode plan at m = 33 (compiled transform phases with five index bytes per fold
+    table, k_dlow): a basis input against the closed-form DFT on sampled amplitudes, and a random
+    slice through transform + inverse back to itself, both under north_star's 1e-12 sqrt(G)."""
+    n = 33
+    x = 0x0_9abc_def1 & ((1 << n) - 1)
+    circ = sv.build_qft(n)
+    fc = sv.FusionConfig(l_c=12, passes=True, exact=False)
+    kinds = [p.kind for p in sv.plan_passes(circ.gates, n, 12, exact=False)]
+    assert kinds.count("local_stage2") >= 3, kinds
+    st = sv.LocalState(sv.Layout(n), big33.a)
+    _lib.check(_lib.load().sv_init_basis(big33.a.data_ptr(), n, x, stream()))
+    sv.run_circuit(st, circ, fusion=fc)
+    rng = np.random.default_rng(6)
+    ks = np.unique(np.concatenate([rng.integers(0, 1 << n, 4096), [0, 1, (1 << n) - 1, 1 << (n - 1)]]))
+    got = big33.a[torch.from_numpy(ks).to(DEV)].cpu().numpy()
+    want = np.empty(len(ks), dtype=np.complex128)
+    for i, k in enumerate(ks.tolist()):
+        rev = int(format(k, f"0{n}b")[::-1], 2)
+        want[i] = np.exp(2j * np.pi * ((x * rev) % (1 << n)) / (1 << n)) / np.sqrt(float(1 << n))
+    err = float(np.max(np.abs(got - want)))
+    assert err <= 1e-12 * np.sqrt(len(circ)), err
+    assert abs(sv.global_norm_sq(st) - 1.0) < 1e-10
+    # random slice: transform then inverse transform (compiled inverse phases) restores it
+    big33.reset()
+    h0 = checksum(big33.a)
+    sv.run_circuit(st, circ, fusion=fc)
+    assert checksum(big33.a) != h0
+    sv.run_circuit(st, circ.inverse(), fusion=fc)
+    probe = torch.from_numpy(ks).to(DEV)
+    back = big33.a[probe].cpu().numpy()
+    big33.reset()
+    orig = big33.a[probe].cpu().numpy()
+    assert float(np.max(np.abs(back - orig))) <= 1e-12 * np.sqrt(2 * len(circ))
