@@ -462,8 +462,9 @@ KERNELS = {
     "pass-local_stage": ("sv_apply_gates:stage", "k_mstage (sv_apply_gates, multi-target stage pass)"),
     "pass-local_tile": ("sv_apply_gates:tile", "k_tile (sv_apply_gates, register-tiled run)"),
     "pass-local_gate": ("sv_apply_single", "k_pairs/k_shfl (single gate of a pass plan)"),
-    "pass-local_stage2": ("sv_apply_gates:dstage2", "k_dstage2 (tolerance mode: eight stage targets per pass, two "
-                                                     "k_dstage programs around a shared-memory transpose)"),
+    "pass-local_stage2": ("sv_apply_gates:dstage2", "k_xstage2 / k_dstage2 (tolerance mode: eight stage targets per "
+                                                     "pass, two phases around a shared-memory transpose; compiled "
+                                                     "phases for transform-shaped groups, the op interpreter otherwise)"),
     "pass-local_low": ("sv_apply_gates:low", "k_dlow (tolerance mode: gates on qubits 0..5, diagonal runs as "
                                             "64-entry product tables)"),
     "pass-local_stage_tol": ("sv_apply_gates:dstage", "k_dstage (tolerance mode: diagonal runs folded into "

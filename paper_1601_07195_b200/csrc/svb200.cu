@@ -1488,102 +1488,11 @@ __device__ __forceinline__ uint64_t spread4(int v, const int32_t (&bits)[MS_K]) 
 // the next tile's phase-1 elements stream into it (cp.async, each thread its own column)
 // while phase 2 computes and stores.  PT carries the tile geometry (s1, s2, lb, tb, scale);
 // F1 / F2 run the two phases on a thread's 16 registers.
-#ifndef SV_DS2_SPLIT
-// 1: the prefetch buffer (64 KiB, thread-private columns) is separate from the transpose buffer,
-// which holds HALF a tile (32 KiB): the next tile streams in during the whole of this one instead
-// of only during phase 2.  The CTA's even and odd warps (the two values of the top coalescing
-// bit) take turns on the transpose buffer through named barriers, so one half transposes while
-// the other computes.  0: one 64 KiB buffer for both (prefetch issued after the transpose).
-// Measured, QFT(30) compiled passes: 8.33 / 8.19 / 8.24 ms (0) vs 8.87 / 7.79 / 7.84 ms (1; the
-// 128-B runs cost the pass on the highest qubits what the longer prefetch gains): off.
-#define SV_DS2_SPLIT 0
-#endif
-constexpr int DS2_SMEM = (SV_DS2_SPLIT ? 6144 : 4096) * (int)sizeof(double2);
+// (A variant with a separate 64 KiB prefetch buffer and a half-tile transpose buffer shared by the
+// CTA's even and odd warps through named barriers -- the next tile in flight during the whole of
+// this one -- measured slower: QFT(30) compiled passes 9.1-9.4 ms vs 6.7-7.2 ms; removed.)
+constexpr int DS2_SMEM = 4096 * (int)sizeof(double2);
 
-__device__ __forceinline__ void bar_sync_n(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-__device__ __forceinline__ void bar_arrive_n(int id, int n) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-
-#if SV_DS2_SPLIT
-template <class PT, class F1, class F2>
-__device__ __forceinline__ void ds2_tiles(double2 *__restrict__ a, uint64_t ntiles, const PT &P, double2 *smem,
-                                          F1 phase1, F2 phase2) {
-  double2 *pb = smem;         // prefetch: row j, column t
-  double2 *xb = smem + 4096;  // transpose of one half: lo3 | s1 << 3 | s2 << 7
-  const int t = threadIdx.x, lane = t & 31, w = t >> 5, half = w & 1;
-  // lo bit 3 is the warp-uniform half; lanes 0..7 keep 128-B runs
-  const int lo = (lane & 7) | (half << 3), hi = (lane >> 3) | ((w >> 1) << 2), lo3 = lane & 7;
-  uint64_t b1[MS_K], b2[MS_K];
-#pragma unroll
-  for (int k = 0; k < MS_K; ++k) b1[k] = 1ull << P.s1[k], b2[k] = 1ull << P.s2[k];
-  const uint64_t lpart = spread4(lo, P.lb);
-  const uint64_t part1 = lpart | spread4(hi, P.s2), part2 = lpart | spread4(hi, P.s1);
-  auto cta_base = [&](uint64_t id) {
-    uint64_t cta = id;
-#pragma unroll
-    for (int k = 0; k < 3 * MS_K; ++k) cta = insert_zero(cta, P.tb[k]);
-    return cta;
-  };
-  // barriers: 1 / 2 = inside half 0 / 1 (128 threads); 3 = half 0 has read the buffer (half 1
-  // may write); 4 = half 1 has read it (half 0 may write)
-  uint64_t id = blockIdx.x;
-  uint64_t cta = cta_base(id);
-  if (id < ntiles) {
-#pragma unroll
-    for (int j = 0; j < MS_N; ++j) cp_async16(&pb[j * 256 + t], a + (cta | part1 | ms_off(j, b1)));
-  }
-  cp_async_commit();
-  if (half == 1 && id < ntiles) bar_arrive_n(4, 256);  // the buffer starts free for half 0
-  for (; id < ntiles; id += gridDim.x) {
-    const uint64_t base1 = cta | part1, base2 = cta | part2;
-    const uint64_t nid = id + gridDim.x;
-    const uint64_t ncta = cta_base(nid);
-    typename F1::Prep f1;
-    phase1.prep(base1, f1);
-    double2 r[MS_N];
-    cp_async_wait_all();
-#pragma unroll
-    for (int j = 0; j < MS_N; ++j) r[j] = pb[j * 256 + t];
-    if (nid < ntiles) {  // the column is private to this thread: refill it at once
-#pragma unroll
-      for (int j = 0; j < MS_N; ++j) cp_async16(&pb[j * 256 + t], a + (ncta | part1 | ms_off(j, b1)));
-    }
-    cp_async_commit();
-    phase1.run(r, base1, f1);
-    typename F2::Prep f2;
-    if (half == 0) {
-      bar_sync_n(4, 256);  // half 1 is done reading
-#pragma unroll
-      for (int j = 0; j < MS_N; ++j) xb[lo3 | (j << 3) | (hi << 7)] = r[j];
-      phase2.prep(base2, f2);
-      bar_sync_n(1, 128);
-#pragma unroll
-      for (int j = 0; j < MS_N; ++j) r[j] = xb[lo3 | (hi << 3) | (j << 7)];
-      bar_arrive_n(3, 256);
-    } else {
-      bar_sync_n(3, 256);  // half 0 is done reading
-#pragma unroll
-      for (int j = 0; j < MS_N; ++j) xb[lo3 | (j << 3) | (hi << 7)] = r[j];
-      phase2.prep(base2, f2);
-      bar_sync_n(2, 128);
-#pragma unroll
-      for (int j = 0; j < MS_N; ++j) r[j] = xb[lo3 | (hi << 3) | (j << 7)];
-      if (nid < ntiles) bar_arrive_n(4, 256);  // not after the last tile: half 0 will not wait again
-    }
-    phase2.run(r, base2, f2);
-    if (P.scale != 1.0) {
-      const double sc = P.scale;
-#pragma unroll
-      for (int j = 0; j < MS_N; ++j) r[j] = make_double2(r[j].x * sc, r[j].y * sc);
-    }
-#pragma unroll
-    for (int j = 0; j < MS_N; ++j) a[base2 | ms_off(j, b2)] = r[j];
-    cta = ncta;
-  }
-  cp_async_wait_all();
-}
-#else
 template <class PT, class F1, class F2>
 __device__ __forceinline__ void ds2_tiles(double2 *__restrict__ a, uint64_t ntiles, const PT &P, double2 *tile,
                                           F1 phase1, F2 phase2) {
@@ -1600,13 +1509,16 @@ __device__ __forceinline__ void ds2_tiles(double2 *__restrict__ a, uint64_t ntil
     return cta;
   };
   uint64_t id = blockIdx.x;
-  uint64_t cta = cta_base(id);
   if (id < ntiles) {
+    const uint64_t cta0 = cta_base(id);
 #pragma unroll
-    for (int j = 0; j < MS_N; ++j) cp_async16(&tile[j * 256 + t], a + (cta | part1 | ms_off(j, b1)));
+    for (int j = 0; j < MS_N; ++j) cp_async16(&tile[j * 256 + t], a + (cta0 | part1 | ms_off(j, b1)));
   }
   cp_async_commit();
   for (; id < ntiles; id += gridDim.x) {
+    // the tile base is recomputed here and for the prefetch below rather than carried: carried,
+    // ptxas spills it and every warp waits ~12 % of its time on the reload before the stores
+    const uint64_t cta = cta_base(id);
     const uint64_t base1 = cta | part1, base2 = cta | part2;
     // a phase's per-thread factors are fetched while its registers are not live yet (the
     // prefetched column still in flight; the tile in shared memory between the transposes)
@@ -1627,8 +1539,8 @@ __device__ __forceinline__ void ds2_tiles(double2 *__restrict__ a, uint64_t ntil
     for (int j = 0; j < MS_N; ++j) r[j] = tile[lo | (hi << 4) | (j << 8)];
     __syncthreads();  // the transpose is read: the buffer takes the next tile
     const uint64_t nid = id + gridDim.x;
-    const uint64_t ncta = cta_base(nid);
     if (nid < ntiles) {
+      const uint64_t ncta = cta_base(nid);
 #pragma unroll
       for (int j = 0; j < MS_N; ++j) cp_async16(&tile[j * 256 + t], a + (ncta | part1 | ms_off(j, b1)));
     }
@@ -1641,12 +1553,10 @@ __device__ __forceinline__ void ds2_tiles(double2 *__restrict__ a, uint64_t ntil
     }
 #pragma unroll
     for (int j = 0; j < MS_N; ++j) a[base2 | ms_off(j, b2)] = r[j];
-    cta = ncta;
   }
   cp_async_wait_all();
 }
 
-#endif
 
 // the interpreter as a ds2_tiles phase: nothing to prepare
 template <int NB>
