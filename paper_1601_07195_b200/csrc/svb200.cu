@@ -1049,8 +1049,37 @@ __device__ __forceinline__ uint64_t ms_off(int j, const uint64_t (&b)[MS_K]) {
   return o;
 }
 
-// The speculative run (all 32 lanes of the warp take part).
-__device__ __forceinline__ void ms_run(double2 (&r)[MS_N], uint64_t base, const MsParams &P) {
+// A stage group shaped like transform stages (the reference's build_qft, circuits.py:141-156),
+// compiled: for slots s descending -- the slot's uncontrolled Hadamard-like gate, its phase gates
+// controlled by the lower slots (descending), then its phase gates controlled from outside the
+// slots (runs rlo..rhi-1 of MsParams.run) -- in exactly the circuit's order, so every amplitude
+// sees mix()'s rounding sequence as in the dispatched path; only the control flow differs
+// (no per-run switch over 100 specialised loops: 14 code blocks instead).  -1: absent.
+struct XmParams {
+  int32_t h[MS_K];
+  int32_t ins[MS_K][MS_K];
+  int32_t rlo[MS_K], rhi[MS_K];
+};
+
+template <int S>
+__device__ __forceinline__ void xm_slot(double2 (&r)[MS_N], uint64_t base, const MsParams &P, const XmParams &X,
+                                        const uint32_t (&M)[4], const uint32_t (&L)[4]) {
+  if (X.h[S] >= 0) ms_apply<S, MS_K, KIND_HSHARE>(r, P.g[X.h[S]].q);
+  if (S > 2 && X.ins[S][2] >= 0) ms_apply<S, (S > 2 ? 2 : 0), KIND_PHASE>(r, P.g[X.ins[S][2]].q);
+  if (S > 1 && X.ins[S][1] >= 0) ms_apply<S, (S > 1 ? 1 : 0), KIND_PHASE>(r, P.g[X.ins[S][1]].q);
+  if (S > 0 && X.ins[S][0] >= 0) ms_apply<S, (S > 0 ? 0 : 1), KIND_PHASE>(r, P.g[X.ins[S][0]].q);
+  for (int ri = X.rlo[S]; ri < X.rhi[S]; ++ri) {
+    const MsRun R = P.run[ri];
+    const uint32_t mh = R.h == 0 ? M[0] : R.h == 1 ? M[1] : R.h == 2 ? M[2] : M[3];
+    const uint32_t lh = R.h == 0 ? L[0] : R.h == 1 ? L[1] : R.h == 2 ? L[2] : L[3];
+    const uint32_t act = mh & R.range;
+    if (act) ms_loop<S, MS_K, KIND_PHASE>(r, act, lh & R.range, 32 * R.h, base, P);
+  }
+}
+
+// The speculative run (all 32 lanes of the warp take part).  XF: the compiled transform shape.
+template <bool XF>
+__device__ __forceinline__ void ms_run(double2 (&r)[MS_N], uint64_t base, const MsParams &P, const XmParams &X) {
   const int lane = threadIdx.x & 31;
   uint64_t vary = base ^ __shfl_sync(0xffffffffu, base, 0);  // index bits that differ between lanes
   vary = ((uint64_t)__reduce_or_sync(0xffffffffu, (unsigned)(vary >> 32)) << 32) |
@@ -1076,6 +1105,15 @@ __device__ __forceinline__ void ms_run(double2 (&r)[MS_N], uint64_t base, const 
     if (h == 1) M1 = mb, L1 = lb;
     if (h == 2) M2 = mb, L2 = lb;
     if (h == 3) M3 = mb, L3 = lb;
+  }
+  if (XF) {
+    static_assert(MS_K == 4, "compiled stage groups assume four slots");
+    const uint32_t M[4] = {M0, M1, M2, M3}, L[4] = {L0, L1, L2, L3};
+    xm_slot<3>(r, base, P, X, M, L);
+    xm_slot<2>(r, base, P, X, M, L);
+    xm_slot<1>(r, base, P, X, M, L);
+    xm_slot<0>(r, base, P, X, M, L);
+    return;
   }
   for (int ri = 0; ri < P.nruns; ++ri) {
     const MsRun R = P.run[ri];
@@ -1190,9 +1228,11 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 #ifndef SV_MS_THREADS
 #define SV_MS_THREADS (SV_MS_MINB * 256)  // resident threads per SM the register budget must allow
 #endif
+template <bool XF>
 __global__ void __launch_bounds__(MS_BLK, SV_MS_THREADS / MS_BLK) k_mstage(double2 *__restrict__ a,
                                                                           uint64_t ngroups,
-                                                                          const __grid_constant__ MsParams P) {
+                                                                          const __grid_constant__ MsParams P,
+                                                                          const __grid_constant__ XmParams X) {
   const uint64_t p = (uint64_t)blockIdx.x * MS_BLK + threadIdx.x;
   uint64_t b[MS_K], base = p;
 #pragma unroll
@@ -1214,7 +1254,7 @@ __global__ void __launch_bounds__(MS_BLK, SV_MS_THREADS / MS_BLK) k_mstage(doubl
   double2 r[MS_N];
 #pragma unroll
   for (int j = 0; j < MS_N; ++j) r[j] = live ? a[base | ms_off(j, b)] : make_double2(1.0, 1.0);
-  ms_run(r, base, P);
+  ms_run<XF>(r, base, P, X);
   bool ok = true;
 #pragma unroll
   for (int j = 0; j < MS_N; ++j) ok &= nonzero2(r[j]);
@@ -1754,7 +1794,8 @@ __device__ __forceinline__ void dl_gate(double2 (&r)[8], uint32_t pm, const doub
 }
 
 #ifndef SV_DL_PREFETCH
-#define SV_DL_PREFETCH 1  // k_dlow: the next block's elements load before this block's gates
+#define SV_DL_PREFETCH 0  // 1: the next block loads before this block's gates (the 32 extra registers spill at
+// three CTAs per SM and cost a CTA at two: QFT(30) tail 7.17 ms; 0 with four CTAs per SM: 5.96 ms)
 #endif
 
 template <int LAYOUT>
@@ -1791,7 +1832,10 @@ __device__ __forceinline__ void dl_stage(double2 (&r)[8], double2 lf, const doub
   }
 }
 
-__global__ void __launch_bounds__(256, 3) k_dlow(double2 *__restrict__ a, uint64_t nblocks,
+#ifndef SV_DL_MINB
+#define SV_DL_MINB 4
+#endif
+__global__ void __launch_bounds__(256, SV_DL_MINB) k_dlow(double2 *__restrict__ a, uint64_t nblocks,
                                                  const __grid_constant__ DlParams P) {
   __shared__ double2 tab[DL_TABMAX * 64];
   __shared__ double2 xp[8][256];  // one 4 KiB transpose buffer per warp
@@ -2449,6 +2493,72 @@ int stage_sig(const StageParams &P) {
   return 1;
 }
 
+#ifndef SV_XM
+#define SV_XM 1  // compiled exact stage groups (k_mstage<true>) for transform-shaped gate lists
+#endif
+
+// Is the stage group (P already built from gates[0..n)) shaped like transform stages in exactly
+// the order the compiled path executes (see XmParams)?  Fills X.
+bool match_xm(const sv_gate *gates, int n, const MsParams &P, XmParams &X) {
+  memset(&X, 0xFF, sizeof(X));  // every index -1
+  for (int s = 0; s < MS_K; ++s) X.rlo[s] = X.rhi[s] = 0;
+#if !SV_XM
+  return false;
+#endif
+  auto slot = [&](int b) {
+    for (int s = 0; s < MS_K; ++s)
+      if (P.bits[s] == b) return s;
+    return MS_K;
+  };
+  int cur = MS_K, stage = 0, last_in = MS_K;  // stage: 0 nothing yet / H seen, 1 in-slot phases, 2 outside phases
+  int glo[MS_K], ghi[MS_K];
+  for (int s = 0; s < MS_K; ++s) glo[s] = ghi[s] = -1;
+  for (int k = 0; k < n; ++k) {
+    const sv_gate &g = gates[k];
+    const int s = slot(g.target), kind = gate_kind(g.q), c = g.control, cs = c >= 0 ? slot(c) : MS_K;
+    if (s == MS_K) return false;
+    if (s != cur) {
+      if (s > cur) return false;  // slots strictly descending, each one block
+      cur = s;
+      stage = 0;
+      last_in = s;
+      if (kind == KIND_HSHARE && c < 0) {
+        X.h[s] = k;
+        continue;
+      }
+    }
+    if (kind != KIND_PHASE || c < 0) return false;
+    if (cs < MS_K) {  // in-slot: lower slots, strictly descending, before the outside ones
+      if (stage > 1 || cs >= last_in) return false;
+      stage = 1;
+      last_in = cs;
+      X.ins[s][cs] = k;
+    } else {
+      if (stage < 2) glo[s] = k;
+      stage = 2;
+      ghi[s] = k + 1;
+    }
+  }
+  // the outside gates of a slot share one code: they are covered by consecutive runs
+  for (int s = 0; s < MS_K; ++s) {
+    if (glo[s] < 0) continue;
+    int lo = -1, hi = -1;
+    for (int ri = 0; ri < P.nruns; ++ri) {
+      const int first = 32 * P.run[ri].h + P.run[ri].lo, last = 32 * P.run[ri].h + P.run[ri].hi;
+      if (first >= glo[s] && last < ghi[s]) {
+        if (lo < 0) lo = ri;
+        hi = ri + 1;
+      } else if (!(last < glo[s] || first >= ghi[s])) {
+        return false;  // a run straddles the range (cannot happen: runs never mix codes)
+      }
+    }
+    if (lo < 0) return false;
+    X.rlo[s] = lo;
+    X.rhi[s] = hi;
+  }
+  return true;
+}
+
 // One multi-target stage launch: gates[0..n) with targets in <= MS_K bits.
 int run_mstage(double2 *a, int m, const sv_gate *gates, int n, cudaStream_t st) {
   static thread_local MsParams P;
@@ -2549,7 +2659,11 @@ int run_mstage(double2 *a, int m, const sv_gate *gates, int n, cudaStream_t st) 
     R.range = (R.hi == 31 ? 0xffffffffu : ((2u << R.hi) - 1u)) & ~((1u << R.lo) - 1u);
   }
   const uint64_t ng = 1ull << (m - MS_K);
-  k_mstage<<<grid_for(ng, MS_BLK), MS_BLK, 0, st>>>(a, ng, P);
+  XmParams X;
+  if (match_xm(gates, n, P, X))
+    k_mstage<true><<<grid_for(ng, MS_BLK), MS_BLK, 0, st>>>(a, ng, P, X);
+  else
+    k_mstage<false><<<grid_for(ng, MS_BLK), MS_BLK, 0, st>>>(a, ng, P, X);
   return after_launch("k_mstage");
 }
 
