@@ -96,8 +96,11 @@ int sv_apply_gates(void *amps, int m, const sv_gate *gates, int ngates, int tile
 /* Slice bits a register tile gathers (its top tile bits; the rest are runs of 2^(tile-8) amplitudes). */
 #define SV_TILE_GATHER 8
 #define SV_GROUP_STAGE 2 /* stage: targets in <= SV_MSTAGE_MAX_TARGETS qubits, 16 amplitudes per thread */
-#define SV_GROUP_LOW 3   /* tolerance mode only: every target in qubits 0..5 (one warp per 256 amplitudes,
-                          * diagonal runs inside the block as one product table) */
+#define SV_GROUP_LOW 3   /* every target in qubits 0..5 (k_dlow: one warp per 256 amplitudes, two register
+                          * layouts switched through a warp-private transpose).  Exact mode: speculative
+                          * structure-specialised updates + one zero test + exact replay, bitwise equal to
+                          * per-gate execution; tolerance mode: diagonal runs inside the block as product
+                          * tables / per-stage factors, deferred butterfly factors */
 #define SV_GROUP_STAGE2 4 /* tolerance mode only: <= 4 targets, then <= 4 others (a 4096-amplitude tile
                            * per CTA, two k_dstage programs around a shared-memory transpose) */
 

@@ -1777,6 +1777,11 @@ struct DlParams {
   int32_t nst, pad;
   double2 stl[DL_TABMAX][8];
   double2 str[DL_TABMAX][4];
+  // exact mode, the tail of a transform (stages t = t0..0 of build_qft, circuits.py:141-156: H(t),
+  // then R(t, c) for c = t-1..0): xq[t] = index in q[] of H(t) (-1: stage absent); the program
+  // then runs as straight-line code (dl_xtail) and hdr[] only serves the exact replay
+  int32_t compiled, pad2;
+  int32_t xq[DL_BITS];
 };
 
 __device__ __forceinline__ int dl_x(int layout, int lane, int j) {  // slice bits 0..7 of (lane, reg j)
@@ -1790,6 +1795,15 @@ __device__ __forceinline__ void dl_gate(double2 (&r)[8], uint32_t pm, const doub
   for (int k = 0; k < 4; ++k) {
     const int j = ((k >> RB) << (RB + 1)) | (k & ((1 << RB) - 1));
     if ((pm >> j) & 1u) spec_pair<KIND>(r[j], r[j | (1 << RB)], q);
+  }
+}
+
+template <int RB>
+__device__ __forceinline__ void dl_gate_exact(double2 (&r)[8], uint32_t pm, const double *q) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int j = ((k >> RB) << (RB + 1)) | (k & ((1 << RB) - 1));
+    if ((pm >> j) & 1u) pair_update<KIND_GENERAL>(r[j], r[j | (1 << RB)], q);
   }
 }
 
@@ -1832,11 +1846,161 @@ __device__ __forceinline__ void dl_stage(double2 (&r)[8], double2 lf, const doub
   }
 }
 
+// ---- the compiled exact transform tail (same updates as the interpreted exact program, in order)
+template <int RB>
+__device__ __forceinline__ void xl_h(double2 (&r)[8], const double *q) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int j = ((k >> RB) << (RB + 1)) | (k & ((1 << RB) - 1));
+    spec_pair<KIND_HSHARE>(r[j], r[j | (1 << RB)], q);
+  }
+}
+// phase on register bit RB controlled by register bit CB / by a lane predicate
+template <int RB, int CB>
+__device__ __forceinline__ void xl_ph_reg(double2 (&r)[8], const double *q) {
+  const double qr = q[6], qi = q[7];
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    if (((j >> RB) & 1) && ((j >> CB) & 1)) r[j] = cmul(qr, qi, r[j]);
+}
+template <int RB>
+__device__ __forceinline__ void xl_ph_lane(double2 (&r)[8], const double *q, bool on) {
+  if (!on) return;
+  const double qr = q[6], qi = q[7];
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    if ((j >> RB) & 1) r[j] = cmul(qr, qi, r[j]);
+}
+
+__device__ __forceinline__ int dl_xtail(double2 (&r)[8], const DlParams &P, double2 *buf, int lane) {
+  const bool l2 = lane & 4, l1 = lane & 2, l0 = lane & 1;  // slice bits 2, 1, 0 in layout H
+  if (P.xq[5] >= 0) {
+    const int g = P.xq[5];
+    xl_h<2>(r, P.q[g]);
+    xl_ph_reg<2, 1>(r, P.q[g + 1]);
+    xl_ph_reg<2, 0>(r, P.q[g + 2]);
+    xl_ph_lane<2>(r, P.q[g + 3], l2);
+    xl_ph_lane<2>(r, P.q[g + 4], l1);
+    xl_ph_lane<2>(r, P.q[g + 5], l0);
+  }
+  if (P.xq[4] >= 0) {
+    const int g = P.xq[4];
+    xl_h<1>(r, P.q[g]);
+    xl_ph_reg<1, 0>(r, P.q[g + 1]);
+    xl_ph_lane<1>(r, P.q[g + 2], l2);
+    xl_ph_lane<1>(r, P.q[g + 3], l1);
+    xl_ph_lane<1>(r, P.q[g + 4], l0);
+  }
+  if (P.xq[3] >= 0) {
+    const int g = P.xq[3];
+    xl_h<0>(r, P.q[g]);
+    xl_ph_lane<0>(r, P.q[g + 1], l2);
+    xl_ph_lane<0>(r, P.q[g + 2], l1);
+    xl_ph_lane<0>(r, P.q[g + 3], l0);
+  }
+  if (P.xq[2] < 0 && P.xq[1] < 0 && P.xq[0] < 0) return 0;
+  dl_transpose<0>(r, buf, lane);  // registers on slice bits 0, 1, 2
+  if (P.xq[2] >= 0) {
+    const int g = P.xq[2];
+    xl_h<2>(r, P.q[g]);
+    xl_ph_reg<2, 1>(r, P.q[g + 1]);
+    xl_ph_reg<2, 0>(r, P.q[g + 2]);
+  }
+  if (P.xq[1] >= 0) {
+    const int g = P.xq[1];
+    xl_h<1>(r, P.q[g]);
+    xl_ph_reg<1, 0>(r, P.q[g + 1]);
+  }
+  if (P.xq[0] >= 0) xl_h<0>(r, P.q[P.xq[0]]);
+  return 1;
+}
+
+// The op program of one warp's block.  REPLAY: every gate through mix() itself (pair_update
+// <KIND_GENERAL>), the exact pass of the bitwise mode; returns the final layout.
+template <bool REPLAY>
+__device__ __forceinline__ int dl_run(double2 (&r)[8], const DlParams &P, const double2 *tab, const double2 *stl,
+                                      double2 *buf, int lane, uint64_t base) {
+  int layout = 0;
+  for (int i = 0; i < P.nops; ++i) {
+    const uint64_t h = P.hdr[i];
+    const int type = (int)(h & 3u), idx = (int)((h >> 16) & 0xffffu);
+    if (type == DL_LAYOUT) {
+      if (layout)
+        dl_transpose<1>(r, buf, lane);
+      else
+        dl_transpose<0>(r, buf, lane);
+      layout = idx;
+      continue;
+    }
+    if (type == DL_TABLE) {
+      if (REPLAY) continue;  // exact programs have no tables
+      if (layout)
+        dl_table<1>(r, tab + idx * 64, lane);
+      else
+        dl_table<0>(r, tab + idx * 64, lane);
+      continue;
+    }
+    if (type == DL_STAGE) {
+      if (REPLAY) continue;
+      const double2 lf = stl[idx * 8 + (lane & 7)];
+      const int rbt = (int)((h >> 2) & 3u);
+      if (rbt == 0)
+        dl_stage<0>(r, lf, P.str[idx]);
+      else if (rbt == 1)
+        dl_stage<1>(r, lf, P.str[idx]);
+      else
+        dl_stage<2>(r, lf, P.str[idx]);
+      continue;
+    }
+    const int cmode = (int)((h >> 8) & 3u), cbit = (int)((h >> 10) & 63u);
+    uint32_t pm = 0xffu;
+    if (cmode == 1) {
+      pm = cbit == 0 ? 0xAAu : cbit == 1 ? 0xCCu : 0xF0u;  // registers whose bit cbit is set
+    } else if (cmode == 2) {
+      const int x0 = dl_x(layout, lane, 0);  // this lane's bits; cbit is not a register bit here
+      const bool on = cbit < 8 ? ((x0 >> cbit) & 1) : ((base >> cbit) & 1ull);
+      if (!on) continue;
+    }
+    const double *q = P.q[idx];
+    const int rb = (int)((h >> 2) & 3u), kind = (int)((h >> 4) & 15u);
+    if (REPLAY) {
+      if (rb == 0)
+        dl_gate_exact<0>(r, pm, q);
+      else if (rb == 1)
+        dl_gate_exact<1>(r, pm, q);
+      else
+        dl_gate_exact<2>(r, pm, q);
+      continue;
+    }
+    switch (rb * 8 + kind) {
+#define DL_CASE(RB_, K_) \
+  case (RB_)*8 + (K_): dl_gate<RB_, K_>(r, pm, q); break;
+#define DL_KINDS(RB_) DL_CASE(RB_, KIND_GENERAL) DL_CASE(RB_, KIND_DIAG) DL_CASE(RB_, KIND_PHASE) \
+  DL_CASE(RB_, KIND_REAL) DL_CASE(RB_, KIND_HSHARE) DL_CASE(RB_, KIND_HBF)
+      DL_KINDS(0) DL_KINDS(1) DL_KINDS(2)
+#undef DL_KINDS
+#undef DL_CASE
+      default: break;
+    }
+  }
+  return layout;
+}
+
 #ifndef SV_DL_MINB
 #define SV_DL_MINB 4
 #endif
-__global__ void __launch_bounds__(256, SV_DL_MINB) k_dlow(double2 *__restrict__ a, uint64_t nblocks,
-                                                 const __grid_constant__ DlParams P) {
+// EXACT (the bitwise mode: a program of GATE / LAYOUT ops only, no tables, no deferred factors):
+// the structure-specialised updates differ from mix() only in the sign of a zero, so the warp tests
+// its final block once and, on any zero component, reloads the block (nothing is stored yet) and
+// replays the program through mix() -- the scheme of k_tile / k_mstage (see "speculative pair updates").
+#ifndef SV_DL_MINB_EXACT
+// CTAs per SM of the exact variant (it carries the replay): 4 / 3 / 2 -> 64 / 80 / 125 registers,
+// 128 / 64 / 0 B of spills, QFT(30) tail 8.46 / 8.45 / 5.95 ms
+#define SV_DL_MINB_EXACT 2
+#endif
+template <bool EXACT>
+__global__ void __launch_bounds__(256, EXACT ? SV_DL_MINB_EXACT : SV_DL_MINB) k_dlow(double2 *__restrict__ a, uint64_t nblocks,
+                                                         const __grid_constant__ DlParams P) {
   __shared__ double2 tab[DL_TABMAX * 64];
   __shared__ double2 xp[8][256];  // one 4 KiB transpose buffer per warp
   __shared__ double2 stl[DL_TABMAX * 8];
@@ -1867,59 +2031,17 @@ __global__ void __launch_bounds__(256, SV_DL_MINB) k_dlow(double2 *__restrict__ 
 #pragma unroll
     for (int j = 0; j < 8; ++j) r[j] = a[base + dl_x(0, lane, j)];
 #endif
-    int layout = 0;
-    for (int i = 0; i < P.nops; ++i) {
-      const uint64_t h = P.hdr[i];
-      const int type = (int)(h & 3u), idx = (int)((h >> 16) & 0xffffu);
-      if (type == DL_LAYOUT) {
-        if (layout)
-          dl_transpose<1>(r, buf, lane);
-        else
-          dl_transpose<0>(r, buf, lane);
-        layout = idx;
-        continue;
+    int layout = (EXACT && P.compiled) ? dl_xtail(r, P, buf, lane) : dl_run<false>(r, P, tab, stl, buf, lane, base);
+    if (EXACT) {
+      bool ok = true;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) ok &= nonzero2(r[j]);
+      if (__any_sync(0xffffffffu, !ok)) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) r[j] = a[base + dl_x(0, lane, j)];
+        layout = dl_run<true>(r, P, tab, stl, buf, lane, base);
       }
-      if (type == DL_TABLE) {
-        if (layout)
-          dl_table<1>(r, tab + idx * 64, lane);
-        else
-          dl_table<0>(r, tab + idx * 64, lane);
-        continue;
-      }
-      if (type == DL_STAGE) {
-        const double2 lf = stl[idx * 8 + (lane & 7)];
-        const int rbt = (int)((h >> 2) & 3u);
-        if (rbt == 0)
-          dl_stage<0>(r, lf, P.str[idx]);
-        else if (rbt == 1)
-          dl_stage<1>(r, lf, P.str[idx]);
-        else
-          dl_stage<2>(r, lf, P.str[idx]);
-        continue;
-      }
-      const int cmode = (int)((h >> 8) & 3u), cbit = (int)((h >> 10) & 63u);
-      uint32_t pm = 0xffu;
-      if (cmode == 1) {
-        pm = cbit == 0 ? 0xAAu : cbit == 1 ? 0xCCu : 0xF0u;  // registers whose bit cbit is set
-      } else if (cmode == 2) {
-        const int x0 = dl_x(layout, lane, 0);  // this lane's bits; cbit is not a register bit here
-        const bool on = cbit < 8 ? ((x0 >> cbit) & 1) : ((base >> cbit) & 1ull);
-        if (!on) continue;
-      }
-      const double *q = P.q[idx];
-      const int rb = (int)((h >> 2) & 3u), kind = (int)((h >> 4) & 15u);
-      switch (rb * 8 + kind) {
-#define DL_CASE(RB_, K_) \
-  case (RB_)*8 + (K_): dl_gate<RB_, K_>(r, pm, q); break;
-#define DL_KINDS(RB_) DL_CASE(RB_, KIND_GENERAL) DL_CASE(RB_, KIND_DIAG) DL_CASE(RB_, KIND_PHASE) \
-  DL_CASE(RB_, KIND_REAL) DL_CASE(RB_, KIND_HSHARE) DL_CASE(RB_, KIND_HBF)
-        DL_KINDS(0) DL_KINDS(1) DL_KINDS(2)
-#undef DL_KINDS
-#undef DL_CASE
-        default: break;
-      }
-    }
-    if (P.scale != 1.0) {
+    } else if (P.scale != 1.0) {
 #pragma unroll
       for (int j = 0; j < 8; ++j) r[j] = make_double2(r[j].x * P.scale, r[j].y * P.scale);
     }
@@ -3124,7 +3246,7 @@ static_assert(DS_MAX >= 3 * MS_MAX / 2 + MS_K && DS_QMAX >= 8 * MS_MAX, "k_dstag
 static_assert(DT_SLOT_BYTES >= (size_t)DS_MAXG * 2 * ((62 + 7) / 8) * 256 * sizeof(double2), "fold-table slot");
 
 // Tolerance-mode low-bit launch (k_dlow): every target in slice bits 0..5 (controls anywhere).
-int run_dlow(double2 *a, int m, const sv_gate *gates, int n, cudaStream_t st) {
+int run_dlow(double2 *a, int m, const sv_gate *gates, int n, cudaStream_t st, bool exact = false) {
   static thread_local DlParams P;
   if (m < 11) return fail(SV_EINVAL, "low-bit group: m=%d below 11", m);
   if (n < 1 || n > DL_MAX) return fail(SV_EINVAL, "low-bit group: %d gates not in [1, %d]", n, DL_MAX);
@@ -3186,7 +3308,7 @@ int run_dlow(double2 *a, int m, const sv_gate *gates, int n, cudaStream_t st) {
     if (g.target < 0 || g.target >= DL_BITS) return fail(SV_EINVAL, "low-bit group: target %d >= %d", g.target, DL_BITS);
     const int c = g.control, kind = gate_kind(g.q);
     const bool diag = kind == KIND_DIAG || kind == KIND_PHASE;
-    if (diag && c < DL_BITS) {  // into the block's product table
+    if (!exact && diag && c < DL_BITS) {  // into the block's product table
       for (int x = 0; x < 64; ++x) {
         if (c >= 0 && !((x >> c) & 1)) continue;
         const int o = ((x >> g.target) & 1) ? 6 : 0;
@@ -3212,7 +3334,7 @@ int run_dlow(double2 *a, int m, const sv_gate *gates, int n, cudaStream_t st) {
       layout ^= 1;
       P.hdr[nops++] = (uint64_t)DL_LAYOUT | ((uint64_t)layout << 16);
     }
-    const bool hbf = kind == KIND_HSHARE && c < 0;
+    const bool hbf = !exact && kind == KIND_HSHARE && c < 0;
     if (hbf) scale *= g.q[0];
     uint64_t cm = 0, cb = 0;
     if (c >= 0) {
@@ -3231,16 +3353,39 @@ int run_dlow(double2 *a, int m, const sv_gate *gates, int n, cudaStream_t st) {
   P.ntab = ntab;
   P.nst = nst;
   P.scale = scale;
+  // exact mode: the gate list is exactly the stages t0..0 of a transform -> the compiled tail
+  P.compiled = 0;
+  for (int t = 0; t < DL_BITS; ++t) P.xq[t] = -1;
+  if (exact) {
+    int k = 0, t = gates[0].target;
+    bool ok = t < DL_BITS;
+    for (; ok && t >= 0; --t) {
+      ok = k < n && gates[k].target == t && gates[k].control < 0 && gate_kind(gates[k].q) == KIND_HSHARE;
+      if (!ok) break;
+      P.xq[t] = k++;
+      for (int c = t - 1; ok && c >= 0; --c, ++k)
+        ok = k < n && gates[k].target == t && gates[k].control == c && gate_kind(gates[k].q) == KIND_PHASE;
+    }
+    P.compiled = (ok && k == n) ? 1 : 0;
+    if (!P.compiled)
+      for (int q = 0; q < DL_BITS; ++q) P.xq[q] = -1;
+  }
   const uint64_t nblocks = 1ull << (m - 8);
-  static int per = 0, nsm = 0;
-  if (!per) {
+  static int per[2] = {0, 0}, nsm = 0;
+  if (!per[exact]) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_dlow, 256, 0) != cudaSuccess || per < 1) per = 1;
+    int v = 0;
+    const cudaError_t e = exact ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_dlow<true>, 256, 0)
+                                : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_dlow<false>, 256, 0);
+    per[exact] = (e != cudaSuccess || v < 1) ? 1 : v;
   }
-  const unsigned grid = (unsigned)std::min<uint64_t>(grid_for(nblocks, 8), (uint64_t)nsm * per);
-  k_dlow<<<grid, 256, 0, st>>>(a, nblocks, P);
+  const unsigned grid = (unsigned)std::min<uint64_t>(grid_for(nblocks, 8), (uint64_t)nsm * per[exact]);
+  if (exact)
+    k_dlow<true><<<grid, 256, 0, st>>>(a, nblocks, P);
+  else
+    k_dlow<false><<<grid, 256, 0, st>>>(a, nblocks, P);
   return after_launch("k_dlow");
 }
 
@@ -3269,14 +3414,14 @@ double stage_cost(const sv_gate &g, bool tol) {
 
 // Tolerance mode: the run from i whose targets all lie in slice bits 0..DL_BITS-1 (k_dlow), as
 // long as its diagonal runs fit the table budget; its length.
-int low_run(int m, const sv_gate *gates, int n, int i) {
+int low_run(int m, const sv_gate *gates, int n, int i, bool tol = true) {
   if (m < 11) return 0;
   int j = i, tabs = 0;
   bool in_diag = false;
   for (; j < n && j - i < DL_MAX; ++j) {
     if (gates[j].target >= DL_BITS) break;
     const int k = gate_kind(gates[j].q);
-    const bool d = (k == KIND_DIAG || k == KIND_PHASE) && gates[j].control < DL_BITS;
+    const bool d = tol && (k == KIND_DIAG || k == KIND_PHASE) && gates[j].control < DL_BITS;
     if (d && !in_diag) {
       if (tabs == DL_TABMAX) break;
       ++tabs;
@@ -3365,12 +3510,14 @@ int next_group(int m, const sv_gate *gates, int n, int i, int T, int *kind, bool
   int lowest = 64;
   for (int k = 0; k < ns; ++k) lowest = S[k] < lowest ? S[k] : lowest;
   if (lowest < 3) cs = 1.7 * pass(cs);  // slot bits 0..2: 16-B pieces at 128-B strides per load (measured)
-  if (tol) {  // a low-bit run at least as long as both other candidates: one k_dlow pass
-    const int C = low_run(m, gates, n, i);
+  {  // a low-bit run at least as long as both other candidates: one k_dlow pass (either mode)
+    const int C = low_run(m, gates, n, i, tol);
     if (C >= 2 && C >= A && C >= B) {
       *kind = SV_GROUP_LOW;
       return i + C;
     }
+  }
+  if (tol) {
     // a two-phase stage run (eight targets) longer than both: one k_dstage2 pass, when it is
     // mostly diagonal (its folds are what make it cheap; general gates cost the same anywhere)
     int split;
@@ -3421,10 +3568,7 @@ bool stage_gains_from_tolerance(const sv_gate *gates, int n) {
 }
 
 int exec_group(double2 *a, int m, int T, int kind, const sv_gate *gates, int n, cudaStream_t st, bool tol = false) {
-  if (kind == SV_GROUP_LOW) {
-    if (!tol) return fail(SV_EINVAL, "low-bit groups run in the tolerance mode only (SV_FLAG_TOLERANCE)");
-    return run_dlow(a, m, gates, n, st);
-  }
+  if (kind == SV_GROUP_LOW) return run_dlow(a, m, gates, n, st, !tol);
   if (kind == SV_GROUP_STAGE2) {
     if (!tol) return fail(SV_EINVAL, "two-phase stage groups run in the tolerance mode only (SV_FLAG_TOLERANCE)");
     int split;

@@ -13,9 +13,10 @@ def test_qft_plan_is_one_pass_per_four_stages():
     circ = sv.build_qft(n)
     plan = sv.plan_passes(circ.gates, m, 12)
     # four consecutive transform stages H(k), R(k, c) for all c < k share one stage pass; the
-    # last six (targets 0..5: a strided stage plus a leftover pass otherwise) are one register tile
+    # last six (targets 0..5: a strided stage plus a leftover pass otherwise) are one low-bit pass
+    # (k_dlow<exact>: one warp per 256 amplitudes)
     assert sv._lib.SV_MSTAGE_MAX_TARGETS == 4
-    assert [p.kind for p in plan] == ["local_stage"] * 6 + ["local_tile"]
+    assert [p.kind for p in plan] == ["local_stage"] * 6 + ["local_low"]
     assert [sorted({op.target for op in p.gates}) for p in plan] == (
         [[k - 3, k - 2, k - 1, k] for k in range(29, 6, -4)] + [list(range(6))])
     assert [op for p in plan for op in p.gates] == list(circ.gates)
@@ -90,6 +91,8 @@ def test_native_planner_invariants(m, seed, tile):
             assert len({t for t in targets if t >= T - G}) <= G
         elif p.kind == "local_stage":
             assert len(targets) <= sv._lib.SV_MSTAGE_MAX_TARGETS and 1 < len(p.gates) <= sv._lib.SV_MSTAGE_MAX_GATES
+        elif p.kind == "local_low":  # every target in qubits 0..5: one k_dlow pass
+            assert max(targets) < 6 and len(p.gates) >= 2
         else:
             assert p.kind == "local_gate"
 
