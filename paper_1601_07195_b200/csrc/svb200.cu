@@ -1228,12 +1228,16 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 #ifndef SV_MS_THREADS
 #define SV_MS_THREADS (SV_MS_MINB * 256)  // resident threads per SM the register budget must allow
 #endif
+#ifndef SV_MS_BLK_XF
+#define SV_MS_BLK_XF 128  // CTA size of the compiled variant: 128 / 256 -> QFT(30) 55.0 / 56.2 ms (same box)
+#endif
 template <bool XF>
-__global__ void __launch_bounds__(MS_BLK, SV_MS_THREADS / MS_BLK) k_mstage(double2 *__restrict__ a,
-                                                                          uint64_t ngroups,
-                                                                          const __grid_constant__ MsParams P,
-                                                                          const __grid_constant__ XmParams X) {
-  const uint64_t p = (uint64_t)blockIdx.x * MS_BLK + threadIdx.x;
+constexpr int ms_blk() { return XF ? SV_MS_BLK_XF : MS_BLK; }
+template <bool XF>
+__global__ void __launch_bounds__(ms_blk<XF>(), SV_MS_THREADS / ms_blk<XF>()) k_mstage(
+    double2 *__restrict__ a, uint64_t ngroups, const __grid_constant__ MsParams P,
+    const __grid_constant__ XmParams X) {
+  const uint64_t p = (uint64_t)blockIdx.x * ms_blk<XF>() + threadIdx.x;
   uint64_t b[MS_K], base = p;
 #pragma unroll
   for (int s = 0; s < MS_K; ++s) b[s] = 1ull << P.bits[s];
@@ -2783,9 +2787,9 @@ int run_mstage(double2 *a, int m, const sv_gate *gates, int n, cudaStream_t st) 
   const uint64_t ng = 1ull << (m - MS_K);
   XmParams X;
   if (match_xm(gates, n, P, X))
-    k_mstage<true><<<grid_for(ng, MS_BLK), MS_BLK, 0, st>>>(a, ng, P, X);
+    k_mstage<true><<<grid_for(ng, ms_blk<true>()), ms_blk<true>(), 0, st>>>(a, ng, P, X);
   else
-    k_mstage<false><<<grid_for(ng, MS_BLK), MS_BLK, 0, st>>>(a, ng, P, X);
+    k_mstage<false><<<grid_for(ng, ms_blk<false>()), ms_blk<false>(), 0, st>>>(a, ng, P, X);
   return after_launch("k_mstage");
 }
 
