@@ -205,3 +205,50 @@ def test_low_group_rejects_high_targets():
     a = torch.zeros(1 << 12, dtype=torch.complex128, device=DEV)
     with pytest.raises(Exception):
         apply_low(a, [sv.GateOp(sv.hadamard(), 7), sv.GateOp(sv.hadamard(), 1)])
+
+
+# ------------------------------------------- compiled stage groups (k_mstage<true>) and their fallbacks
+
+def _transform_stage_group(n, slots, rng, drop=0.0, shuffle_in_slot=False, extra=None):
+    """H(t), R(t, c) for all c < t, for t in `slots` (descending): the stage group of build_qft
+    (circuits.py:141-156) on arbitrary slot qubits, optionally with gates dropped at random."""
+    ops = []
+    for t in sorted(slots, reverse=True):
+        block = [sv.GateOp(sv.hadamard(), t)]
+        ctl = list(range(t - 1, -1, -1))
+        if shuffle_in_slot:
+            rng.shuffle(ctl)
+        block += [sv.GateOp(sv.phase_r(t - c + 1), t, c) for c in ctl]
+        ops += [g for g in block if rng.random() >= drop]
+    if extra is not None:
+        ops.insert(int(rng.integers(len(ops) + 1)), extra)
+    return ops
+
+
+@pytest.mark.parametrize("n,slots", [(14, [13, 12, 11, 10]), (16, [15, 14, 13, 12]), (18, [12, 11, 10, 9]),
+                                     (15, [14, 9, 8, 3]), (20, [19, 18, 17]), (13, [12, 11]), (17, [8, 7, 6, 5])])
+def test_compiled_stage_groups_bitwise(n, slots):
+    """Transform-shaped stage groups take the compiled control flow (k_mstage<true>); with gates
+    dropped, reordered or a foreign gate inserted they either still match or fall back to the
+    dispatched kernel -- every variant bitwise equal to the oracle, on dense, zero-salted and
+    basis states."""
+    rng = np.random.default_rng(5200 + 17 * n + sum(slots))
+    variants = [
+        _transform_stage_group(n, slots, rng),
+        _transform_stage_group(n, slots, rng, drop=0.3),
+        _transform_stage_group(n, slots, rng, drop=0.6),
+        _transform_stage_group(n, slots, rng, shuffle_in_slot=True),
+        _transform_stage_group(n, slots, rng, extra=sv.GateOp(sv.random_unitary(rng), slots[0])),
+        _transform_stage_group(n, slots, rng, extra=sv.GateOp(sv.phase_r(3), slots[-1], slots[0])),
+    ]
+    basis = np.zeros(1 << n, dtype=np.complex128)
+    basis[int(rng.integers(1 << n))] = 1.0
+    for vi, ops in enumerate(variants):
+        ops = ops[:128]
+        if len(ops) < 2:
+            continue
+        for v in (random_state(rng, n), with_zeros(rng, n), basis):
+            a = torch.from_numpy(v.copy()).to(DEV)
+            apply_stage(a, ops)
+            torch.cuda.synchronize()
+            assert bits_equal(a.cpu().numpy(), run_oracle(v, ops)), (n, slots, vi)
