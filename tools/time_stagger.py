@@ -1,7 +1,9 @@
-"""Times the exact pass-fused workloads (config-4-shape random steps, QFT) for the first-wave
-stagger experiment; the stagger comes from SVB_TILE_STAGGER / SVB_MS_STAGGER (cycles per slot).
+"""Times the exact pass-fused workloads (config-4-shape random steps, a 16-gate tile, QFT): the
+A/B timing behind tools/ab_qft.sh.  (Written for the first-wave stagger experiment of round 2 --
+profiles/r02_probes.md section 3; the SVB_TILE_STAGGER / SVB_MS_STAGGER switches it echoed no
+longer exist in the library.)
 
-    SVB_TILE_STAGGER=8000 python tools/time_stagger.py [n] [reps]
+    python tools/time_stagger.py [n] [reps]
 """
 import json
 import os
