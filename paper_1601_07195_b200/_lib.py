@@ -33,7 +33,7 @@ EXPORTS = (
     "sv_exchange_stage", "sv_norm_sq", "sv_init_random", "sv_scale", "sv_init_basis",
     "sv_copy", "sv_ipc_handle", "sv_ipc_open", "sv_ipc_close", "sv_diag_global", "sv_diag_fix",
     "sv_swap_global", "sv_max_abs_diff", "sv_apply_gates_ex", "sv_plan_gates_ex", "sv_apply_group_ex",
-    "sv_pair_update", "sv_stage2_shape",
+    "sv_pair_update", "sv_stage2_shape", "sv_stage_shape",
 )
 
 
@@ -79,6 +79,7 @@ def load() -> ctypes.CDLL:
                               ctypes.POINTER(ctypes.c_int32), i], i),
         "sv_apply_group_ex": ([vp, i, i, ctypes.POINTER(SvGate), i, i, i, vp], i),
         "sv_stage2_shape": ([i, ctypes.POINTER(SvGate), i], i),
+        "sv_stage_shape": ([i, ctypes.POINTER(SvGate), i], i),
         "sv_exchange": ([vp, vp, i, i, i, dp, vp], i),
         "sv_exchange_chunk": ([vp, vp, i, i, i, dp, u64, u64, vp], i),
         "sv_pair_update": ([vp, vp, u64, i, dp, vp], i),

@@ -2686,8 +2686,9 @@ bool match_xm(const sv_gate *gates, int n, const MsParams &P, XmParams &X) {
 }
 
 // One multi-target stage launch: gates[0..n) with targets in <= MS_K bits.
-int run_mstage(double2 *a, int m, const sv_gate *gates, int n, cudaStream_t st) {
-  static thread_local MsParams P;
+// Host part of a stage launch: MsParams (slots, runs, lane layout) and, for a transform-shaped
+// group, the compiled plan X (*compiled = 1).
+int build_mstage(int m, const sv_gate *gates, int n, MsParams &P, XmParams &X, int *compiled) {
   if (n < 1 || n > MS_MAX) return fail(SV_EINVAL, "stage group: %d gates not in [1, %d]", n, MS_MAX);
   if (m < MS_K) return fail(SV_EINVAL, "stage group: m=%d below %d", m, MS_K);
   int bits[MS_K], nb = 0;
@@ -2784,9 +2785,18 @@ int run_mstage(double2 *a, int m, const sv_gate *gates, int n, cudaStream_t st) 
     MsRun &R = P.run[ri];
     R.range = (R.hi == 31 ? 0xffffffffu : ((2u << R.hi) - 1u)) & ~((1u << R.lo) - 1u);
   }
-  const uint64_t ng = 1ull << (m - MS_K);
+  *compiled = match_xm(gates, n, P, X) ? 1 : 0;
+  return SV_OK;
+}
+
+int run_mstage(double2 *a, int m, const sv_gate *gates, int n, cudaStream_t st) {
+  static thread_local MsParams P;
   XmParams X;
-  if (match_xm(gates, n, P, X))
+  int compiled = 0;
+  const int rc = build_mstage(m, gates, n, P, X, &compiled);
+  if (rc != SV_OK) return rc;
+  const uint64_t ng = 1ull << (m - MS_K);
+  if (compiled)
     k_mstage<true><<<grid_for(ng, ms_blk<true>()), ms_blk<true>(), 0, st>>>(a, ng, P, X);
   else
     k_mstage<false><<<grid_for(ng, ms_blk<false>()), ms_blk<false>(), 0, st>>>(a, ng, P, X);
@@ -3750,6 +3760,18 @@ int sv_plan_gates_ex(int m, const sv_gate *gates, int ngates, int tile, int flag
     ++ng;
   }
   return ng;
+}
+
+int sv_stage_shape(int m, const sv_gate *gates, int ngates) {
+  if (!gates) return fail(SV_EINVAL, "sv_stage_shape: null pointer");
+  if (m < 1 || m > 62 || ngates < 1) return fail(SV_EINVAL, "sv_stage_shape: m=%d / ngates=%d invalid", m, ngates);
+  int rc = check_gates("sv_stage_shape", m, gates, ngates, m);
+  if (rc != SV_OK) return rc;
+  static thread_local MsParams P;
+  XmParams X;
+  int compiled = 0;
+  rc = build_mstage(m, gates, ngates, P, X, &compiled);
+  return rc != SV_OK ? rc : (compiled ? SV_SHAPE_FORWARD : SV_SHAPE_INTERPRETED);
 }
 
 int sv_stage2_shape(int m, const sv_gate *gates, int ngates) {

@@ -127,3 +127,34 @@ def test_fusion_config_passes_flag_keeps_reference_plans():
     assert not ref.passes and all(isinstance(s, (sv.FusedBlockRun, sv.PassThrough)) for s in ref.segments)
     p = sv.plan_fusion(circ, sv.FusionConfig(l_c=5, passes=True))
     assert p.passes and p.flatten() == list(circ.gates)
+
+
+def test_transform_stage_groups_take_the_compiled_path():
+    """sv_stage_shape (pure host): the exact planner's stage groups of build_qft
+    (circuits.py:141-156) are recognised as transform stages in circuit order (k_mstage with
+    compiled control flow); a group with a foreign gate, or with a stage's phases out of
+    order, stays with the run-dispatched kernel."""
+    from paper_1601_07195_b200 import _lib
+    from paper_1601_07195_b200.kernels import gate_array
+
+    def shape(m, gates):
+        gates = list(gates)
+        return _lib.load().sv_stage_shape(m, gate_array(gates), len(gates))
+
+    for n in (18, 26, 30, 33):
+        groups = [p for p in sv.plan_passes(sv.build_qft(n).gates, n, 12) if p.kind == "local_stage"]
+        assert groups
+        assert all(shape(n, p.gates) == _lib.SV_SHAPE_FORWARD for p in groups)
+    n = 26
+    gates = list([p for p in sv.plan_passes(sv.build_qft(n).gates, n, 12) if p.kind == "local_stage"][0].gates)
+    rng = np.random.default_rng(0)
+    foreign = gates[:5] + [sv.GateOp(sv.random_unitary(rng), gates[0].target)] + gates[5:]
+    assert shape(n, foreign) == _lib.SV_SHAPE_INTERPRETED
+    swapped = gates[:]
+    swapped[1], swapped[2] = swapped[2], swapped[1]  # the in-slot phases of the first stage out of order
+    assert shape(n, swapped) == _lib.SV_SHAPE_INTERPRETED
+    dropped = [g for k, g in enumerate(gates) if k % 7 != 3]  # still stages in order
+    assert shape(n, dropped) == _lib.SV_SHAPE_FORWARD
+    # inverse transform: not the forward shape (runs dispatched)
+    inv = [p for p in sv.plan_passes(sv.build_qft(n).inverse().gates, n, 12) if p.kind == "local_stage"]
+    assert inv and all(shape(n, p.gates) == _lib.SV_SHAPE_INTERPRETED for p in inv)
