@@ -171,3 +171,37 @@ def test_two_phase_stage_groups_mixed_diagonals():
     v = random_state(rng, n)
     got, want = run_both(n, circ, v)
     assert float(np.max(np.abs(got - want))) <= bound(len(circ))
+
+
+@pytest.mark.parametrize("n,l_c,seed", [(14, 12, 21), (16, 11, 22), (17, 12, 23), (19, 12, 24), (20, 10, 25)])
+def test_scheduled_mixed_circuits_tolerance(n, l_c, seed):
+    """Merged and reordered gates (passes.schedule_gates) through the tolerance kernels: Haar gates,
+    Hadamards, (controlled) phase rotations and general diagonals on random placements -- the
+    commutation-aware order must leave the state within the bound of the original order's."""
+    rng = np.random.default_rng(seed)
+    ops = []
+    for _ in range(260):
+        t = int(rng.integers(n))
+        c = int((t + 1 + rng.integers(n - 1)) % n)
+        kind = rng.random()
+        if kind < 0.3:
+            ops.append(sv.GateOp(sv.random_unitary(rng), t))
+        elif kind < 0.5:
+            ops.append(sv.GateOp(sv.random_unitary(rng), t, c))
+        elif kind < 0.6:
+            ops.append(sv.GateOp(sv.hadamard(), t))
+        elif kind < 0.8:
+            ops.append(sv.GateOp(sv.phase_r(int(rng.integers(2, 9))), t, c))
+        elif kind < 0.9:
+            ops.append(sv.GateOp(sv.phase_r(int(rng.integers(2, 9))), t))
+        else:
+            d = sv.GateMatrix.unchecked(np.diag(np.exp(1j * rng.uniform(0, 2 * np.pi, 2))))
+            ops.append(sv.GateOp(d, t, c if rng.random() < 0.5 else None))
+    circ = sv.Circuit(n, ops)
+    fc = sv.FusionConfig(l_c=l_c, passes=True, exact=False)
+    exact_plan = sv.plan_passes(circ.gates, n, sv.passes.tile_for(l_c, n))
+    tol_plan = sv.plan_passes(circ.gates, n, sv.passes.tile_for(l_c, n), exact=False)
+    assert len(tol_plan) <= len(exact_plan)
+    v = random_state(rng, n)
+    got, want = run_both(n, circ, v, fusion=fc)
+    assert float(np.max(np.abs(got - want))) <= bound(len(circ))
