@@ -1750,6 +1750,61 @@ __global__ void __launch_bounds__(256, SV_DS2_MINB) k_xstage2(double2 *__restric
   ds2_tiles(a, ntiles, P, tile, XfRun<NB, INV, FULL>{P.ph[0], P.tab}, XfRun<NB, INV, FULL>{P.ph[1], P.tab});
 }
 
+// The single-phase form (a tolerance stage group of at most four targets shaped like transform
+// stages): k_dstage's persistent, column-prefetching skeleton around one compiled phase.
+struct Xf1Params {
+  int32_t nbytes, pad;
+  int32_t bits[MS_K];
+  double scale;
+  const double2 *tab;
+  XfPhase ph;
+};
+
+template <int NB, bool INV>
+__global__ void __launch_bounds__(256, SV_DS_MINB) k_xstage(double2 *__restrict__ a, uint64_t ngroups,
+                                                           const __grid_constant__ Xf1Params P) {
+  extern __shared__ double2 stage_smem[];  // [MS_N][256]: this thread's slots are a column
+  double2(*stage)[256] = reinterpret_cast<double2(*)[256]>(stage_smem);
+  const int tid = threadIdx.x;
+  uint64_t b[MS_K];
+#pragma unroll
+  for (int s = 0; s < MS_K; ++s) b[s] = 1ull << P.bits[s];
+  const uint64_t stride = (uint64_t)gridDim.x * 256;
+  uint64_t p = (uint64_t)blockIdx.x * 256 + tid;
+  const XfRun<NB, INV, false> phase{P.ph, P.tab};
+  if (p < ngroups) {
+    const uint64_t base = ds_base(p, P.bits);
+#pragma unroll
+    for (int j = 0; j < MS_N; ++j) cp_async16(&stage[j][tid], a + (base | ms_off(j, b)));
+  }
+  cp_async_commit();
+  for (; p < ngroups; p += stride) {
+    const uint64_t base = ds_base(p, P.bits);
+    typename XfRun<NB, INV, false>::Prep f;
+    phase.prep(base, f);
+    double2 r[MS_N];
+    cp_async_wait_all();
+#pragma unroll
+    for (int j = 0; j < MS_N; ++j) r[j] = stage[j][tid];
+    const uint64_t pn = p + stride;
+    if (pn < ngroups) {
+      const uint64_t nbase = ds_base(pn, P.bits);
+#pragma unroll
+      for (int j = 0; j < MS_N; ++j) cp_async16(&stage[j][tid], a + (nbase | ms_off(j, b)));
+    }
+    cp_async_commit();
+    phase.run(r, base, f);
+    if (P.scale != 1.0) {
+      const double sc = P.scale;
+#pragma unroll
+      for (int j = 0; j < MS_N; ++j) r[j] = make_double2(r[j].x * sc, r[j].y * sc);
+    }
+#pragma unroll
+    for (int j = 0; j < MS_N; ++j) a[base | ms_off(j, b)] = r[j];
+  }
+  cp_async_wait_all();
+}
+
 // ------------------------------ tolerance-mode low-bit passes (targets in slice bits 0..5)
 //
 // One warp per 256-amplitude block (slice bits 0..7); each lane holds 8 elements in one of
@@ -3188,6 +3243,34 @@ int run_dstage2(double2 *a, int m, const sv_gate *gates, int n, int split, cudaS
   return after_launch("k_dstage2");
 }
 
+template <int NB, bool INV>
+int launch_xstage_t(double2 *a, int m, const Xf1Params &X, cudaStream_t st) {
+  constexpr int SMEM = MS_N * 256 * (int)sizeof(double2);
+  static int per = 0, nsm = 0;
+  if (!per) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(k_xstage<NB, INV>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_xstage<NB, INV>, 256, SMEM) != cudaSuccess || per < 1)
+      per = 1;
+  }
+  const uint64_t ng = 1ull << (m - MS_K);
+  const unsigned grid = (unsigned)std::min<uint64_t>(grid_for(ng, 256), (uint64_t)nsm * per);
+  k_xstage<NB, INV><<<grid, 256, SMEM, st>>>(a, ng, X);
+  return after_launch("k_xstage");
+}
+
+template <bool INV>
+int launch_xstage(double2 *a, int m, const Xf1Params &X, cudaStream_t st) {
+  switch (X.nbytes) {
+    case 2: return launch_xstage_t<2, INV>(a, m, X, st);
+    case 3: return launch_xstage_t<3, INV>(a, m, X, st);
+    case 4: return launch_xstage_t<4, INV>(a, m, X, st);
+    default: return launch_xstage_t<5, INV>(a, m, X, st);
+  }
+}
+
 // Tolerance-mode stage launch (k_dtable + k_dstage): compile gates[0..n) (targets in <= MS_K
 // bits) into GATE / FLUSH ops and fold groups.
 int run_dstage(double2 *a, int m, const sv_gate *gates, int n, cudaStream_t st) {
@@ -3199,6 +3282,23 @@ int run_dstage(double2 *a, int m, const sv_gate *gates, int n, cudaStream_t st) 
   int rc = ds_slots(gates, n, m, 0, bits);
   if (rc) return rc;
   const int nbytes = (m + 7) / 8;
+#if SV_XFORM
+  if (nbytes >= 2 && nbytes <= 5) {  // shaped like transform stages: the compiled phase
+    static thread_local Xf1Params X;
+    for (int inverse = 0; inverse < 2; ++inverse) {
+      T.nfold = 0;
+      int ng = 0;
+      double scale = 1.0;
+      if (!match_xform(gates, n, bits, inverse != 0, X.ph, T, &ng, &scale)) continue;
+      rc = launch_dtable(T, ng, nbytes, st, &X.tab);
+      if (rc) return rc;
+      X.nbytes = nbytes;
+      X.scale = scale;
+      for (int k = 0; k < MS_K; ++k) X.bits[k] = bits[k];
+      return inverse ? launch_xstage<true>(a, m, X, st) : launch_xstage<false>(a, m, X, st);
+    }
+  }
+#endif
   int ngroups = 0;
   bool has0[DS_MAXG] = {};
   T.nfold = 0;
@@ -3460,6 +3560,9 @@ int stage2_run(int m, const sv_gate *gates, int n, int i, int *split) {
   };
   for (; j < n; ++j) {
     const int t = gates[j].target;
+    // slots below bit 4 would push the coalescing lanes off the contiguous low bits (such a pass
+    // runs at 1.5-2.3x an ordinary one): those gates are left to a low-bit pass / a stage pass
+    if (t < MS_K) break;
     if (ph == 0 && !in(0, t)) {
       if (ns[0] == MS_K) {
         ph = 1;
@@ -3530,13 +3633,26 @@ int next_group(int m, const sv_gate *gates, int n, int i, int T, int *kind, bool
       *kind = SV_GROUP_LOW;
       return i + C;
     }
+    // tolerance mode: k_dlow is one HBM-bound pass whatever it carries (diagonal runs are
+    // factors), so it also wins against a longer but FP64-heavy tile / stage run per gate --
+    // e.g. the first stages of an inverse transform (a 78-gate tile of 12 stages: 24 ms at
+    // n = 30; its first six stages as a low-bit pass: 6 ms)
+    if (tol && C >= 8) {
+      const double per_low = 5.5 / C;
+      if ((A <= 1 || per_low <= pass(ct) / A) && (B <= 1 || per_low <= pass(cs) / B)) {
+        *kind = SV_GROUP_LOW;
+        return i + C;
+      }
+    }
   }
   if (tol) {
     // a two-phase stage run (eight targets) longer than both: one k_dstage2 pass, when it is
     // mostly diagonal (its folds are what make it cheap; general gates cost the same anywhere)
     int split;
     const int e = stage2_run(m, gates, n, i, &split);
-    if (e - i > B && e - i >= A) {
+    // longer than the stage run, and longer than the tile run or cheaper per gate than it (a
+    // mostly diagonal two-phase pass costs ~7 ms whatever it carries)
+    if (e - i > B && (e - i >= A || 7.0 / (e - i) <= pass(ct) / A)) {
       int nd = 0;
       for (int k = i; k < e; ++k) {
         const int kd = gate_kind(gates[k].q);

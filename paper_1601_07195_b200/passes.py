@@ -175,6 +175,41 @@ def schedule_gates(ops, tile: int, gather: int = _lib.SV_TILE_GATHER) -> list[Ga
     return [ops[g] for g in order]
 
 
+def _gate_class(op: GateOp) -> str:
+    """general / diagonal / real / hadamard-like, as the native planner's cost model sees a gate."""
+    mat = np.asarray(_as_gate(op.gate).mat)
+    if mat[0, 1] == 0 and mat[1, 0] == 0:
+        return "diag"
+    if np.any(mat.imag != 0):
+        return "general"
+    return "hlike" if mat[0, 0] == mat[0, 1] == mat[1, 0] == -mat[1, 1] else "real"
+
+
+_TILE_COST = {"general": 1.15, "diag": 0.45, "real": 0.75, "hlike": 0.55}
+_STAGE_COST = {"general": 0.9, "diag": 0.02, "real": 0.55, "hlike": 0.35}
+
+
+def plan_cost(plan) -> float:
+    """Estimated milliseconds at 2^30 amplitudes of a tolerance-mode plan of local passes: the
+    native planner's model (svb200.cu next_group: a pass costs max(5, its gates' FP64 time); a
+    low-bit pass 5.5, a mostly diagonal two-phase pass 7).  Only used to choose between the
+    circuit's own order and the scheduled one."""
+    total = 0.0
+    for p in plan:
+        if p.kind == "local_low":
+            total += 5.5
+        elif p.kind == "local_stage2":
+            total += max(7.0, sum(_STAGE_COST[_gate_class(op)] for op in p.gates))
+        elif p.kind == "local_stage":
+            total += max(5.0, sum(_STAGE_COST[_gate_class(op)] * (0.5 if op.control is not None else 1.0)
+                                  for op in p.gates))
+        elif p.kind == "local_tile":
+            total += max(5.0, sum(_TILE_COST[_gate_class(op)] for op in p.gates))
+        else:
+            total += 5.0 * len(p.gates)
+    return total
+
+
 def plan_passes(gates, m: int, tile: int = 0, exact: bool = True) -> list[Pass]:
     """Cut a gate sequence into HBM passes -- a pure function of the gates, m and the tile,
     so every rank derives the same list (the collective fences line up).
@@ -200,9 +235,9 @@ def plan_passes(gates, m: int, tile: int = 0, exact: bool = True) -> list[Pass]:
                 j += 1
             local = _plan_local(gates[i:j], m, tile, exact)
             if not exact and tile >= 9 and len(local) > 1:
-                # the commutation-aware order, when the native planner needs fewer passes for it
+                # the commutation-aware order, when the native planner's passes get cheaper with it
                 again = _plan_local(schedule_gates(gates[i:j], tile), m, tile, exact)
-                if len(again) < len(local):
+                if plan_cost(again) < 0.98 * plan_cost(local):
                     local = again
             out.extend(local)
         i = j
