@@ -161,3 +161,23 @@ def test_two_phase_groups_of_transforms_compile():
     assert _shape(n, broken) == _lib.SV_SHAPE_INTERPRETED
     # not a two-phase group at all: an error, not a shape
     assert _shape(n, gates[:3]) < 0
+
+
+def test_inverse_transform_plan_mirrors_the_forward_one():
+    """Tolerance planner: the inverse of build_qft starts with the low-bit pass on stages 0..5 (not a
+    78-gate tile of twelve stages) and continues with two-phase passes of eight stages; forward
+    plans keep bits 0..3 out of two-phase groups (they end with a low-bit pass)."""
+    for n in (20, 28, 30):
+        fwd = sv.plan_passes(sv.build_qft(n).gates, n, 12, exact=False)
+        inv = sv.plan_passes(sv.build_qft(n).inverse().gates, n, 12, exact=False)
+        assert fwd[-1].kind == "local_low" and inv[0].kind == "local_low"
+        assert len(inv[0].gates) == 21 and {op.target for op in inv[0].gates} == set(range(6))
+        assert all(p.kind in ("local_stage2", "local_stage") for p in inv[1:])
+        assert len(inv) <= len(fwd) + 1
+        for p in fwd:
+            if p.kind == "local_stage2":
+                assert min(op.target for op in p.gates) >= 4
+    # the cost model behind the choices is monotone in the obvious way
+    from paper_1601_07195_b200.passes import plan_cost
+
+    assert plan_cost(sv.plan_passes(sv.build_qft(30).gates, 30, 12, exact=False)) < 35.0
