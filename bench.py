@@ -20,9 +20,10 @@ events on the launching stream, max over ranks.  The 16 GiB slice is ~130x
 the 126 MB L2, so no flush is needed between steps.
 
 The same line carries the BASELINE configs 3 / 4 / 5 shapes as secondary
-objects (``secondary``: config-3 controlled gates per gate with (c, t) buckets,
-config-4-shaped random steps and the config-5 transform through the pass
-planner, exact and tolerance-mode), each with its own roofline.
+objects (``secondary``: config-3 controlled gates per gate with (c, t) buckets
+and through the pass planner, config-4-shaped random steps and the config-5
+transform through the pass planner, exact and tolerance-mode), each with its
+own roofline.
 """
 
 from __future__ import annotations
@@ -667,7 +668,8 @@ def run_ours(args, world, rank, local):
     # ------------------------ secondary objects: BASELINE configs 3 / 4 / 5 shapes, same slice
     secondary = {}
     if not args.no_secondary and args.n is None:
-        plan = [("controlled", "controlled", "none"), ("random_passes", "random", "passes"),
+        plan = [("controlled", "controlled", "none"), ("controlled_passes", "controlled", "passes"),
+                ("random_passes", "random", "passes"),
                 ("random_tolerance", "random", "tolerance"),
                 ("qft_passes", "qft", "passes"), ("qft_tolerance", "qft", "tolerance")]
         for name, wl, fz in plan:
