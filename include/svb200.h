@@ -135,9 +135,10 @@ int sv_apply_group_ex(void *amps, int m, int kind, const sv_gate *gates, int nga
 #define SV_SHAPE_FORWARD 1
 #define SV_SHAPE_INVERSE 2
 int sv_stage2_shape(int m, const sv_gate *gates, int ngates);
-/* The same question for an exact stage group (SV_GROUP_STAGE): SV_SHAPE_FORWARD when the group is
- * transform stages in circuit order (k_mstage with compiled control flow; same arithmetic, same
- * order, bit-identical), SV_SHAPE_INTERPRETED for the run-dispatched kernel.  Pure host code. */
+/* The same question for an exact stage group (SV_GROUP_STAGE): SV_SHAPE_FORWARD / SV_SHAPE_INVERSE when
+ * the group is transform stages (or inverse stages) in circuit order (k_mstage with compiled control
+ * flow; same arithmetic, same order, bit-identical), SV_SHAPE_INTERPRETED for the run-dispatched
+ * kernel.  Pure host code. */
 int sv_stage_shape(int m, const sv_gate *gates, int ngates);
 
 /* Staged variant of sv_exchange for the NCCL data plane (NvlinkFabric(data_plane=

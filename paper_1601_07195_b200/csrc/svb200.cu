@@ -1059,6 +1059,8 @@ struct XmParams {
   int32_t h[MS_K];
   int32_t ins[MS_K][MS_K];
   int32_t rlo[MS_K], rhi[MS_K];
+  int32_t inverse, pad;  // inverse transform stages: slots ascending, each [outside phases, in-slot phases
+                         // (control slots ascending), butterfly]
 };
 
 template <int S>
@@ -1075,6 +1077,22 @@ __device__ __forceinline__ void xm_slot(double2 (&r)[MS_N], uint64_t base, const
     const uint32_t act = mh & R.range;
     if (act) ms_loop<S, MS_K, KIND_PHASE>(r, act, lh & R.range, 32 * R.h, base, P);
   }
+}
+
+template <int S>
+__device__ __forceinline__ void xm_slot_inv(double2 (&r)[MS_N], uint64_t base, const MsParams &P, const XmParams &X,
+                                            const uint32_t (&M)[4], const uint32_t (&L)[4]) {
+  for (int ri = X.rlo[S]; ri < X.rhi[S]; ++ri) {
+    const MsRun R = P.run[ri];
+    const uint32_t mh = R.h == 0 ? M[0] : R.h == 1 ? M[1] : R.h == 2 ? M[2] : M[3];
+    const uint32_t lh = R.h == 0 ? L[0] : R.h == 1 ? L[1] : R.h == 2 ? L[2] : L[3];
+    const uint32_t act = mh & R.range;
+    if (act) ms_loop<S, MS_K, KIND_PHASE>(r, act, lh & R.range, 32 * R.h, base, P);
+  }
+  if (S > 0 && X.ins[S][0] >= 0) ms_apply<S, (S > 0 ? 0 : 1), KIND_PHASE>(r, P.g[X.ins[S][0]].q);
+  if (S > 1 && X.ins[S][1] >= 0) ms_apply<S, (S > 1 ? 1 : 0), KIND_PHASE>(r, P.g[X.ins[S][1]].q);
+  if (S > 2 && X.ins[S][2] >= 0) ms_apply<S, (S > 2 ? 2 : 0), KIND_PHASE>(r, P.g[X.ins[S][2]].q);
+  if (X.h[S] >= 0) ms_apply<S, MS_K, KIND_HSHARE>(r, P.g[X.h[S]].q);
 }
 
 // The speculative run (all 32 lanes of the warp take part).  XF: the compiled transform shape.
@@ -1109,6 +1127,13 @@ __device__ __forceinline__ void ms_run(double2 (&r)[MS_N], uint64_t base, const 
   if (XF) {
     static_assert(MS_K == 4, "compiled stage groups assume four slots");
     const uint32_t M[4] = {M0, M1, M2, M3}, L[4] = {L0, L1, L2, L3};
+    if (X.inverse) {
+      xm_slot_inv<0>(r, base, P, X, M, L);
+      xm_slot_inv<1>(r, base, P, X, M, L);
+      xm_slot_inv<2>(r, base, P, X, M, L);
+      xm_slot_inv<3>(r, base, P, X, M, L);
+      return;
+    }
     xm_slot<3>(r, base, P, X, M, L);
     xm_slot<2>(r, base, P, X, M, L);
     xm_slot<1>(r, base, P, X, M, L);
@@ -1974,6 +1999,52 @@ __device__ __forceinline__ int dl_xtail(double2 (&r)[8], const DlParams &P, doub
   return 1;
 }
 
+// The inverse tail: stages t = 0..t0, each [R(t, c) for c = 0..t-1, then the butterfly]; xq[t] = index of
+// the stage's first gate.  Registers on bits 0, 1, 2 first, then on bits 3, 4, 5 (the store layout).
+__device__ __forceinline__ int dl_xtail_inv(double2 (&r)[8], const DlParams &P, double2 *buf, int lane) {
+  dl_transpose<0>(r, buf, lane);  // registers on slice bits 0, 1, 2
+  if (P.xq[0] >= 0) xl_h<0>(r, P.q[P.xq[0]]);
+  if (P.xq[1] >= 0) {
+    const int g = P.xq[1];
+    xl_ph_reg<1, 0>(r, P.q[g]);
+    xl_h<1>(r, P.q[g + 1]);
+  }
+  if (P.xq[2] >= 0) {
+    const int g = P.xq[2];
+    xl_ph_reg<2, 0>(r, P.q[g]);
+    xl_ph_reg<2, 1>(r, P.q[g + 1]);
+    xl_h<2>(r, P.q[g + 2]);
+  }
+  if (P.xq[3] < 0 && P.xq[4] < 0 && P.xq[5] < 0) return 1;
+  dl_transpose<1>(r, buf, lane);  // registers on slice bits 3, 4, 5
+  const bool l2 = lane & 4, l1 = lane & 2, l0 = lane & 1;
+  if (P.xq[3] >= 0) {
+    const int g = P.xq[3];
+    xl_ph_lane<0>(r, P.q[g], l0);
+    xl_ph_lane<0>(r, P.q[g + 1], l1);
+    xl_ph_lane<0>(r, P.q[g + 2], l2);
+    xl_h<0>(r, P.q[g + 3]);
+  }
+  if (P.xq[4] >= 0) {
+    const int g = P.xq[4];
+    xl_ph_lane<1>(r, P.q[g], l0);
+    xl_ph_lane<1>(r, P.q[g + 1], l1);
+    xl_ph_lane<1>(r, P.q[g + 2], l2);
+    xl_ph_reg<1, 0>(r, P.q[g + 3]);
+    xl_h<1>(r, P.q[g + 4]);
+  }
+  if (P.xq[5] >= 0) {
+    const int g = P.xq[5];
+    xl_ph_lane<2>(r, P.q[g], l0);
+    xl_ph_lane<2>(r, P.q[g + 1], l1);
+    xl_ph_lane<2>(r, P.q[g + 2], l2);
+    xl_ph_reg<2, 0>(r, P.q[g + 3]);
+    xl_ph_reg<2, 1>(r, P.q[g + 4]);
+    xl_h<2>(r, P.q[g + 5]);
+  }
+  return 0;
+}
+
 // The op program of one warp's block.  REPLAY: every gate through mix() itself (pair_update
 // <KIND_GENERAL>), the exact pass of the bitwise mode; returns the final layout.
 template <bool REPLAY>
@@ -2090,7 +2161,9 @@ __global__ void __launch_bounds__(256, EXACT ? SV_DL_MINB_EXACT : SV_DL_MINB) k_
 #pragma unroll
     for (int j = 0; j < 8; ++j) r[j] = a[base + dl_x(0, lane, j)];
 #endif
-    int layout = (EXACT && P.compiled) ? dl_xtail(r, P, buf, lane) : dl_run<false>(r, P, tab, stl, buf, lane, base);
+    int layout = !(EXACT && P.compiled) ? dl_run<false>(r, P, tab, stl, buf, lane, base)
+                 : P.compiled == 2   ? dl_xtail_inv(r, P, buf, lane)
+                                     : dl_xtail(r, P, buf, lane);
     if (EXACT) {
       bool ok = true;
 #pragma unroll
@@ -2680,43 +2753,56 @@ int stage_sig(const StageParams &P) {
 
 // Is the stage group (P already built from gates[0..n)) shaped like transform stages in exactly
 // the order the compiled path executes (see XmParams)?  Fills X.
-bool match_xm(const sv_gate *gates, int n, const MsParams &P, XmParams &X) {
+// forward: slots descending, a block = [butterfly][in-slot phases, control slots descending][outside
+// phases]; inverse: slots ascending, a block = [outside phases][in-slot phases, ascending][butterfly].
+bool match_xm_dir(const sv_gate *gates, int n, const MsParams &P, XmParams &X, bool inverse) {
   memset(&X, 0xFF, sizeof(X));  // every index -1
   for (int s = 0; s < MS_K; ++s) X.rlo[s] = X.rhi[s] = 0;
-#if !SV_XM
-  return false;
-#endif
+  X.inverse = inverse ? 1 : 0;
+  X.pad = 0;
   auto slot = [&](int b) {
     for (int s = 0; s < MS_K; ++s)
       if (P.bits[s] == b) return s;
     return MS_K;
   };
-  int cur = MS_K, stage = 0, last_in = MS_K;  // stage: 0 nothing yet / H seen, 1 in-slot phases, 2 outside phases
+  // phase of a block -- forward: 0 butterfly / nothing yet, 1 in-slot, 2 outside;
+  //                     inverse: 0 outside / nothing yet, 1 in-slot, 2 butterfly seen (closed)
+  int cur = -1, stage = 0, last_in = 0;
   int glo[MS_K], ghi[MS_K];
   for (int s = 0; s < MS_K; ++s) glo[s] = ghi[s] = -1;
   for (int k = 0; k < n; ++k) {
     const sv_gate &g = gates[k];
     const int s = slot(g.target), kind = gate_kind(g.q), c = g.control, cs = c >= 0 ? slot(c) : MS_K;
     if (s == MS_K) return false;
-    if (s != cur) {
-      if (s > cur) return false;  // slots strictly descending, each one block
+    const bool bfly = kind == KIND_HSHARE && c < 0;
+    if (s != cur) {  // a new block: slots strictly descending (forward) / ascending (inverse)
+      if (cur >= 0 && (inverse ? s < cur : s > cur)) return false;
       cur = s;
       stage = 0;
-      last_in = s;
-      if (kind == KIND_HSHARE && c < 0) {
+      last_in = inverse ? -1 : s;
+      if (!inverse && bfly) {
         X.h[s] = k;
         continue;
       }
     }
+    if (inverse && bfly) {
+      if (stage == 2) return false;
+      X.h[s] = k;
+      stage = 2;
+      continue;
+    }
     if (kind != KIND_PHASE || c < 0) return false;
-    if (cs < MS_K) {  // in-slot: lower slots, strictly descending, before the outside ones
-      if (stage > 1 || cs >= last_in) return false;
+    if (inverse && stage == 2) return false;  // nothing of this slot after its butterfly
+    if (cs < MS_K) {  // in-slot: lower slots only, in the order the compiled path applies them
+      if (cs >= s) return false;
+      if (inverse ? cs <= last_in : (stage > 1 || cs >= last_in)) return false;
       stage = 1;
       last_in = cs;
       X.ins[s][cs] = k;
     } else {
-      if (stage < 2) glo[s] = k;
-      stage = 2;
+      if (inverse ? stage != 0 : false) return false;  // inverse: outside phases come first
+      if (glo[s] < 0) glo[s] = k;
+      if (!inverse) stage = 2;
       ghi[s] = k + 1;
     }
   }
@@ -2738,6 +2824,16 @@ bool match_xm(const sv_gate *gates, int n, const MsParams &P, XmParams &X) {
     X.rhi[s] = hi;
   }
   return true;
+}
+
+bool match_xm(const sv_gate *gates, int n, const MsParams &P, XmParams &X) {
+#if SV_XM
+  if (match_xm_dir(gates, n, P, X, false) || match_xm_dir(gates, n, P, X, true)) return true;
+#endif
+  memset(&X, 0xFF, sizeof(X));
+  for (int s = 0; s < MS_K; ++s) X.rlo[s] = X.rhi[s] = 0;
+  X.inverse = 0;
+  return false;
 }
 
 // One multi-target stage launch: gates[0..n) with targets in <= MS_K bits.
@@ -3360,6 +3456,45 @@ static_assert(DS_MAX >= 3 * MS_MAX / 2 + MS_K && DS_QMAX >= 8 * MS_MAX, "k_dstag
 static_assert(DT_SLOT_BYTES >= (size_t)DS_MAXG * 2 * ((62 + 7) / 8) * 256 * sizeof(double2), "fold-table slot");
 
 // Tolerance-mode low-bit launch (k_dlow): every target in slice bits 0..5 (controls anywhere).
+// The tail of a transform on qubits t0..0 (t0 <= 5), exactly: 1 = forward (for t = t0..0: the
+// butterfly, then R(t, c) for c = t-1..0), 2 = inverse (for t = 0..t0: R(t, c) for c = 0..t-1,
+// then the butterfly), 0 = neither; xq[t] = index of stage t's first gate.
+int xtail_shape(const sv_gate *gates, int n, int32_t (&xq)[DL_BITS]) {
+  auto is_h = [&](int k, int t) {
+    return k < n && gates[k].target == t && gates[k].control < 0 && gate_kind(gates[k].q) == KIND_HSHARE;
+  };
+  auto is_r = [&](int k, int t, int c) {
+    return k < n && gates[k].target == t && gates[k].control == c && gate_kind(gates[k].q) == KIND_PHASE;
+  };
+  for (int t = 0; t < DL_BITS; ++t) xq[t] = -1;
+  if (n < 1 || gates[0].target >= DL_BITS) return 0;
+  {  // forward
+    int k = 0, t = gates[0].target;
+    bool ok = true;
+    for (; ok && t >= 0; --t) {
+      ok = is_h(k, t);
+      if (!ok) break;
+      xq[t] = k++;
+      for (int c = t - 1; ok && c >= 0; --c, ++k) ok = is_r(k, t, c);
+    }
+    if (ok && k == n) return 1;
+  }
+  for (int t = 0; t < DL_BITS; ++t) xq[t] = -1;
+  {  // inverse
+    int k = 0;
+    bool ok = gates[0].target == 0;
+    for (int t = 0; ok && t < DL_BITS && k < n; ++t) {
+      xq[t] = k;
+      for (int c = 0; ok && c < t; ++c, ++k) ok = is_r(k, t, c);
+      ok = ok && is_h(k, t);
+      ++k;
+    }
+    if (ok && k == n) return 2;
+  }
+  for (int t = 0; t < DL_BITS; ++t) xq[t] = -1;
+  return 0;
+}
+
 int run_dlow(double2 *a, int m, const sv_gate *gates, int n, cudaStream_t st, bool exact = false) {
   static thread_local DlParams P;
   if (m < 11) return fail(SV_EINVAL, "low-bit group: m=%d below 11", m);
@@ -3467,23 +3602,10 @@ int run_dlow(double2 *a, int m, const sv_gate *gates, int n, cudaStream_t st, bo
   P.ntab = ntab;
   P.nst = nst;
   P.scale = scale;
-  // exact mode: the gate list is exactly the stages t0..0 of a transform -> the compiled tail
-  P.compiled = 0;
-  for (int t = 0; t < DL_BITS; ++t) P.xq[t] = -1;
-  if (exact) {
-    int k = 0, t = gates[0].target;
-    bool ok = t < DL_BITS;
-    for (; ok && t >= 0; --t) {
-      ok = k < n && gates[k].target == t && gates[k].control < 0 && gate_kind(gates[k].q) == KIND_HSHARE;
-      if (!ok) break;
-      P.xq[t] = k++;
-      for (int c = t - 1; ok && c >= 0; --c, ++k)
-        ok = k < n && gates[k].target == t && gates[k].control == c && gate_kind(gates[k].q) == KIND_PHASE;
-    }
-    P.compiled = (ok && k == n) ? 1 : 0;
-    if (!P.compiled)
-      for (int q = 0; q < DL_BITS; ++q) P.xq[q] = -1;
-  }
+  // exact mode: the gate list is exactly the stages t0..0 of a transform (or 0..t0 of its inverse)
+  P.compiled = exact ? xtail_shape(gates, n, P.xq) : 0;
+  if (!P.compiled)
+    for (int q = 0; q < DL_BITS; ++q) P.xq[q] = -1;
   const uint64_t nblocks = 1ull << (m - 8);
   static int per[2] = {0, 0}, nsm = 0;
   if (!per[exact]) {
@@ -3632,6 +3754,16 @@ int next_group(int m, const sv_gate *gates, int n, int i, int T, int *kind, bool
     if (C >= 2 && C >= A && C >= B) {
       *kind = SV_GROUP_LOW;
       return i + C;
+    }
+    // exact mode: a transform tail (forward or inverse) runs as compiled straight-line code in
+    // k_dlow<exact> -- one HBM-bound pass (6 ms at n = 30) where the tile needs 10 ms for the six
+    // forward stages and 24 ms for the twelve inverse stages it would gather
+    if (!tol && C >= 10) {
+      int32_t xq[DL_BITS];
+      if (xtail_shape(gates + i, C, xq)) {
+        *kind = SV_GROUP_LOW;
+        return i + C;
+      }
     }
     // tolerance mode: k_dlow is one HBM-bound pass whatever it carries (diagonal runs are
     // factors), so it also wins against a longer but FP64-heavy tile / stage run per gate --
@@ -3887,7 +4019,7 @@ int sv_stage_shape(int m, const sv_gate *gates, int ngates) {
   XmParams X;
   int compiled = 0;
   rc = build_mstage(m, gates, ngates, P, X, &compiled);
-  return rc != SV_OK ? rc : (compiled ? SV_SHAPE_FORWARD : SV_SHAPE_INTERPRETED);
+  return rc != SV_OK ? rc : (!compiled ? SV_SHAPE_INTERPRETED : X.inverse ? SV_SHAPE_INVERSE : SV_SHAPE_FORWARD);
 }
 
 int sv_stage2_shape(int m, const sv_gate *gates, int ngates) {

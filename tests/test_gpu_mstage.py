@@ -201,6 +201,39 @@ def test_low_group_is_the_transform_tail():
         assert bits_equal(st.to_numpy(), run_oracle(v, list(circ.gates)))
 
 
+def test_inverse_transform_exact_plan_bitwise():
+    """The exact plan of the inverse transform mirrors the forward one -- a compiled low-bit pass on
+    stages 0..5, then compiled inverse stage groups -- and stays bit-identical to per-gate execution
+    on dense, zero-salted and basis inputs; sub-tails (stages 0..t0) too."""
+    from paper_1601_07195_b200 import _lib
+
+    n = 18
+    circ = sv.build_qft(n).inverse()
+    plan = sv.plan_passes(circ.gates, n, 12)
+    assert plan[0].kind == "local_low" and len(plan[0].gates) == 21
+    for p in plan[1:]:
+        assert p.kind == "local_stage"
+        assert _lib.load().sv_stage_shape(n, gate_array(list(p.gates)), len(p.gates)) == _lib.SV_SHAPE_INVERSE
+    rng = np.random.default_rng(78)
+    basis = np.zeros(1 << n, dtype=np.complex128)
+    basis[54321] = 1.0
+    for v in (random_state(rng, n), with_zeros(rng, n), basis):
+        st = sv.state_from_global(sv.Layout(n), v, device=DEV)
+        sv.run_circuit(st, circ, fusion=sv.FusionConfig(l_c=12, passes=True))
+        torch.cuda.synchronize()
+        assert bits_equal(st.to_numpy(), run_oracle(v, list(circ.gates)))
+    for t0 in (1, 2, 3, 4, 5):  # inverse and forward sub-tails as single low-bit groups
+        fwd = [op for op in sv.build_qft(n).gates if op.target <= t0]
+        for ops in (fwd, [op.dagger() for op in reversed(fwd)]):
+            if len(ops) < 2:
+                continue
+            for v in (random_state(rng, 13), with_zeros(rng, 13)):
+                a = torch.from_numpy(v.copy()).to(DEV)
+                apply_low(a, ops)
+                torch.cuda.synchronize()
+                assert bits_equal(a.cpu().numpy(), run_oracle(v, ops)), t0
+
+
 def test_low_group_rejects_high_targets():
     a = torch.zeros(1 << 12, dtype=torch.complex128, device=DEV)
     with pytest.raises(Exception):
@@ -241,6 +274,8 @@ def test_compiled_stage_groups_bitwise(n, slots):
         _transform_stage_group(n, slots, rng, extra=sv.GateOp(sv.random_unitary(rng), slots[0])),
         _transform_stage_group(n, slots, rng, extra=sv.GateOp(sv.phase_r(3), slots[-1], slots[0])),
     ]
+    # the inverse stages (gates reversed and conjugated): the compiled inverse shape and its fallbacks
+    variants += [[op.dagger() for op in reversed(v)] for v in variants[:5]]
     basis = np.zeros(1 << n, dtype=np.complex128)
     basis[int(rng.integers(1 << n))] = 1.0
     for vi, ops in enumerate(variants):

@@ -155,6 +155,11 @@ def test_transform_stage_groups_take_the_compiled_path():
     assert shape(n, swapped) == _lib.SV_SHAPE_INTERPRETED
     dropped = [g for k, g in enumerate(gates) if k % 7 != 3]  # still stages in order
     assert shape(n, dropped) == _lib.SV_SHAPE_FORWARD
-    # inverse transform: not the forward shape (runs dispatched)
-    inv = [p for p in sv.plan_passes(sv.build_qft(n).inverse().gates, n, 12) if p.kind == "local_stage"]
-    assert inv and all(shape(n, p.gates) == _lib.SV_SHAPE_INTERPRETED for p in inv)
+    # inverse transform: the compiled inverse shape, after a compiled low-bit pass on stages 0..5
+    plan = sv.plan_passes(sv.build_qft(n).inverse().gates, n, 12)
+    assert plan[0].kind == "local_low" and len(plan[0].gates) == 21
+    inv = [p for p in plan if p.kind == "local_stage"]
+    assert inv and all(shape(n, p.gates) == _lib.SV_SHAPE_INVERSE for p in inv)
+    # a forward stage list reversed WITHOUT conjugating is still inverse-shaped (phases are phases)
+    rev = list(reversed(gates))
+    assert shape(n, rev) == _lib.SV_SHAPE_INVERSE
