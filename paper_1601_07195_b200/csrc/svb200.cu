@@ -3749,16 +3749,18 @@ int next_group(int m, const sv_gate *gates, int n, int i, int T, int *kind, bool
   int lowest = 64;
   for (int k = 0; k < ns; ++k) lowest = S[k] < lowest ? S[k] : lowest;
   if (lowest < 3) cs = 1.7 * pass(cs);  // slot bits 0..2: 16-B pieces at 128-B strides per load (measured)
-  {  // a low-bit run at least as long as both other candidates: one k_dlow pass (either mode)
+  {  // a low-bit run: one k_dlow pass
     const int C = low_run(m, gates, n, i, tol);
-    if (C >= 2 && C >= A && C >= B) {
+    // tolerance mode: when it is at least as long as both other candidates
+    if (tol && C >= 2 && C >= A && C >= B) {
       *kind = SV_GROUP_LOW;
       return i + C;
     }
-    // exact mode: a transform tail (forward or inverse) runs as compiled straight-line code in
-    // k_dlow<exact> -- one HBM-bound pass (6 ms at n = 30) where the tile needs 10 ms for the six
-    // forward stages and 24 ms for the twelve inverse stages it would gather
-    if (!tol && C >= 10) {
+    // exact mode: only a transform tail (forward or inverse), which runs as compiled straight-line
+    // code in k_dlow<exact> -- one HBM-bound pass (6 ms at n = 30) where the tile needs 10 ms for the
+    // six forward stages and 24 ms for the twelve inverse stages it would gather.  (Any other exact
+    // low-bit run goes through the op interpreter at ~0.8 ms per gate: the tile is faster.)
+    if (!tol && C >= 2 && (C >= 10 || (C >= A && C >= B))) {
       int32_t xq[DL_BITS];
       if (xtail_shape(gates + i, C, xq)) {
         *kind = SV_GROUP_LOW;
