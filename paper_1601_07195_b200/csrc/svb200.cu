@@ -3257,6 +3257,15 @@ int stage2_shape(int m, const sv_gate *gates, int n, int split, const int (&s1)[
   return 0;
 }
 
+// Index bytes the fold tables of a compiled launch really need: up to the highest fold control
+// (the product over higher bytes is 1), at least 2 (the smallest instantiation).
+int fold_bytes(const DtParams &T, int nbytes) {
+  int top = 0;
+  for (int i = 0; i < T.nfold; ++i) top = T.f[i].c > top ? T.f[i].c : top;
+  const int need = top / 8 + 1;
+  return need < 2 ? 2 : need < nbytes ? need : nbytes;
+}
+
 // Two-phase tolerance stage launch (k_dstage2): gates[0..split) target S1, gates[split..n) S2.
 int run_dstage2(double2 *a, int m, const sv_gate *gates, int n, int split, cudaStream_t st) {
   static thread_local Ds2Params P;
@@ -3272,9 +3281,10 @@ int run_dstage2(double2 *a, int m, const sv_gate *gates, int n, int split, cudaS
     double scale = 1.0;
     const int shape = stage2_shape(m, gates, n, split, s1, s2, X, T, &ng, &scale);
     if (shape) {
-      rc = launch_dtable(T, ng, nbytes, st, &X.tab);
+      const int nb = fold_bytes(T, nbytes);  // QFT(30): 4 / 3 / 2 bytes for the three passes
+      rc = launch_dtable(T, ng, nb, st, &X.tab);
       if (rc) return rc;
-      X.nbytes = nbytes;
+      X.nbytes = nb;
       X.scale = scale;
       int xt[3 * MS_K], nx = 0;
       for (int k = 0; k < MS_K; ++k) {
@@ -3386,9 +3396,10 @@ int run_dstage(double2 *a, int m, const sv_gate *gates, int n, cudaStream_t st) 
       int ng = 0;
       double scale = 1.0;
       if (!match_xform(gates, n, bits, inverse != 0, X.ph, T, &ng, &scale)) continue;
-      rc = launch_dtable(T, ng, nbytes, st, &X.tab);
+      const int nb = fold_bytes(T, nbytes);
+      rc = launch_dtable(T, ng, nb, st, &X.tab);
       if (rc) return rc;
-      X.nbytes = nbytes;
+      X.nbytes = nb;
       X.scale = scale;
       for (int k = 0; k < MS_K; ++k) X.bits[k] = bits[k];
       return inverse ? launch_xstage<true>(a, m, X, st) : launch_xstage<false>(a, m, X, st);
